@@ -1,0 +1,350 @@
+#!/usr/bin/env python3
+"""Benchmark of the NLEM / EM-ADMM hot path on B200 (driver contract: one JSON line).
+
+Workload (BASELINE.json metric "denoised Mpixels/s at fixed ADMM iters (7x7 patch,
+21x21 window); % FP32 peak"): config 3 — NLEM denoise of the 4096x4096 synthetic
+image (2000 rectangles, 1500 disks, sigma=30), k=7, S=21, h=10*sigma with the
+BASELINE d*h^2 normalisation (reference h_ref = h*sqrt(d)), box [0,255], mu=1,
+weighted-mean (NLM) init, 10 ADMM sweeps.  One step = one pass of the hot path
+over the rank's row band (strong scaling: the image is split into row bands with
+a 13-row halo over N GPUs, no collective on the data path).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+`value` times the fused kernels with the band resident in HBM (CUDA events on
+the launching stream, max over ranks); `e2e` times the reference-facing host
+call nlem_denoise_rows_host (H2D of the band from pinned memory, kernels, D2H).
+`--impl reference` times the reference algorithm on the host cores (the FP64
+oracle restatement; the reference itself needs Eigen, absent here).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "denoised Mpixels/s at fixed ADMM iters (7x7 patch, 21x21 window); % FP32 peak"
+CFG = dict(rows=4096, cols=4096, rects=2000, disks=1500, sigma=30.0, patch=7, search=21, iters=10,
+           mu=1.0)
+PEAK_FP32_TFLOPS_NOMINAL = 148 * 128 * 2 * 1.965e9 / 1e12  # SMs x lanes x FMA x max clock
+
+
+def band_rows(rows: int, rank: int, world: int):
+    per = (rows + world - 1) // world
+    r0 = min(rows, rank * per)
+    return r0, min(rows, r0 + per) - r0
+
+
+def sum_neighbours(rows, cols, search, r0, nrows):
+    """Sigma_i n_i over the band: clipped window sizes (proj/src/patch.cpp:72-85)."""
+    hs = search // 2
+    r = np.arange(r0, r0 + nrows)
+    c = np.arange(cols)
+    nr = np.minimum(rows - 1, r + hs) - np.maximum(0, r - hs) + 1
+    nc = np.minimum(cols - 1, c + hs) - np.maximum(0, c - hs) + 1
+    return int(nr.sum()) * int(nc.sum())
+
+
+def algorithmic_flops(sum_n, d, T):
+    """ADMM 12*d*T*sum_n + weights 3*d*sum_n + weighted-mean init 2*d*sum_n."""
+    return 12 * d * T * sum_n + 3 * d * sum_n + 2 * d * sum_n
+
+
+class ClockSampler:
+    """NVML SM clock + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int, period=0.1):
+        self.index, self.period = index, period
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            self.error = str(e)
+        return self
+
+    def _run(self):
+        N = self.N
+        names = {
+            getattr(N, "nvmlClocksEventReasonHwSlowdown", 0x8): "hw_slowdown",
+            getattr(N, "nvmlClocksEventReasonSwThermalSlowdown", 0x20): "sw_thermal_slowdown",
+            getattr(N, "nvmlClocksEventReasonHwThermalSlowdown", 0x40): "hw_thermal_slowdown",
+            getattr(N, "nvmlClocksEventReasonSwPowerCap", 0x4): "sw_power_cap",
+            getattr(N, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80): "hw_power_brake_slowdown",
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(self.period)
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def load_profile_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def cpu_reference(noisy, params_kw, sample_rows, threads):
+    """Time the FP64 oracle (restated reference) on a row sample; returns (Mpix/s, seconds)."""
+    from oracle import oracle as O
+
+    o = O.make_params(search=params_kw["search"], patch=params_kw["patch"], h=params_kw["h"],
+                      solver="admm", solver_iters=params_kw["iters"], mu=params_kw["mu"],
+                      init_mode="nlm", box=(0.0, 255.0), threads=threads)
+    X = noisy.astype(np.float64)
+    t0 = time.perf_counter()
+    px = 0
+    for r in sample_rows:
+        O.nlem_denoise(X, o, rows=(r, r + 1))
+        px += X.shape[1]
+    dt = time.perf_counter() - t0
+    return px / dt / 1e6, dt, px
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-sample-rows", type=int, default=6)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    d = CFG["patch"] ** 2
+    h_ref = 10.0 * CFG["sigma"] * math.sqrt(d)
+    threads = os.cpu_count() or 1
+
+    from paper_1501_03879_b200 import synth
+
+    config = {"workload": "BASELINE config 3: NLEM denoise 4096x4096 synthetic, k=7 (d=49), "
+                          "S=21 (n<=441), h=10*sigma (h_ref=2100), box [0,255], mu=1, NLM init, "
+                          "T=10 ADMM sweeps",
+              "rows": CFG["rows"], "cols": CFG["cols"], "sigma": CFG["sigma"], "patch": 7,
+              "search": 21, "iters": CFG["iters"], "parallelism": f"row-bands x{args.gpus}",
+              "halo_rows": 13}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        _, noisy = synth.config_image(3)
+        pkw = dict(search=21, patch=7, h=h_ref, iters=CFG["iters"], mu=CFG["mu"])
+        rows_per_step = 2
+        rng = np.random.default_rng(0)
+        samples = [sorted(rng.choice(CFG["rows"], rows_per_step, replace=False).tolist())
+                   for _ in range(args.warmup + args.steps)]
+        for s in samples[: args.warmup]:
+            cpu_reference(noisy, pkw, s, threads)
+        vals, secs, pxs = [], 0.0, 0
+        for s in samples[args.warmup:]:
+            v, dt, px = cpu_reference(noisy, pkw, s, threads)
+            vals.append(v)
+            secs += dt
+            pxs += px
+        value = pxs / secs / 1e6
+        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixels/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": config,
+                "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": threads,
+                                 "kind": "port",
+                                 "sample": f"{rows_per_step} random full rows (2x4096 px) of the "
+                                           "config-3 image per step, FP64 oracle restatement of "
+                                           "the reference (Eigen absent: reference unbuildable)"},
+                "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    import paper_1501_03879_b200 as nb
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    clean, noisy = synth.config_image(3)
+    rows, cols = CFG["rows"], CFG["cols"]
+    params = nb.NlemParams(search=21, patch=7, h=h_ref, sigma=CFG["sigma"], solver="admm",
+                           solver_iters=CFG["iters"], mu=CFG["mu"], init_mode="nlm")
+    halo = nb.band_halo(params)
+    r0, nrows = band_rows(rows, rank, world)
+    i0, i1 = max(0, r0 - halo), min(rows, r0 + nrows + halo)
+    band_in = np.ascontiguousarray(noisy[i0:i1])
+    X = torch.from_numpy(band_in).cuda()
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # > 126 MB L2
+
+    def step():
+        return nb.nlem_denoise_rows(X, i0, rows, cols, r0, nrows, params)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        out = step()
+    barrier()
+
+    # ---- device-resident timed region
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clocks:
+        barrier()
+        t_all0 = torch.cuda.Event(enable_timing=True)
+        t_all1 = torch.cuda.Event(enable_timing=True)
+        t_all0.record(stream)
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict the band from L2 between steps
+            ev[i][0].record(stream)
+            out = step()
+            ev[i][1].record(stream)
+        t_all1.record(stream)
+        barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = t_all0.elapsed_time(t_all1)
+    kernel_ms = sum(step_ms) / len(step_ms)
+    t = torch.tensor([total_ms, kernel_ms], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kernel_ms_max = t.tolist()
+    ms_per_step = total_ms / args.steps
+
+    # ---- e2e through the host-buffer C-ABI entry (pinned host memory)
+    pin_in = torch.from_numpy(band_in).pin_memory()
+    pin_out = torch.empty((nrows, cols), dtype=torch.float32).pin_memory()
+    pin_in_np, pin_out_np = pin_in.numpy(), pin_out.numpy()
+    nb.nlem_denoise_rows_host(pin_in_np, i0, rows, cols, r0, nrows, params, out=pin_out_np,
+                              device=local)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        nb.nlem_denoise_rows_host(pin_in_np, i0, rows, cols, r0, nrows, params, out=pin_out_np,
+                                  device=local)
+    barrier()
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_s = float(e2e_s.item())
+    assert np.array_equal(pin_out_np, out.cpu().numpy()), "host entry != device entry"
+
+    # ---- gather the full output for a quality line (outside any timed region)
+    if dist is not None:
+        outs = [None] * world
+        dist.all_gather_object(outs, out.cpu().numpy())
+        full = np.concatenate(outs, axis=0) if rank == 0 else None
+    else:
+        full = out.cpu().numpy()
+
+    sum_n_band = sum_neighbours(rows, cols, 21, r0, nrows)
+    flops = algorithmic_flops(sum_n_band, d, CFG["iters"])
+    achieved = flops / (kernel_ms / 1e3) / 1e12  # this rank's kernel
+    achieved_t = torch.tensor([achieved], device="cuda", dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(achieved_t, op=dist.ReduceOp.MIN)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    psnr_noisy = 10 * math.log10(255 ** 2 / float(np.mean((noisy.astype(np.float64) - clean) ** 2)))
+    psnr_out = 10 * math.log10(255 ** 2 / float(np.mean((full.astype(np.float64) - clean) ** 2)))
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        rng = np.random.default_rng(1)
+        sample = sorted(rng.choice(rows, args.cpu_sample_rows, replace=False).tolist())
+        v, dt, px = cpu_reference(noisy, dict(search=21, patch=7, h=h_ref, iters=CFG["iters"],
+                                              mu=CFG["mu"]), sample, threads)
+        cpu = {"value": v, "unit": "Mpixels/s", "cores": threads, "kind": "port",
+               "sample": f"{len(sample)} random full rows ({px} px) of the config-3 image, FP64 "
+                         f"oracle restatement, {dt:.1f} s"}
+
+    value = rows * cols / (total_ms / args.steps / 1e3) / 1e6
+    e2e_val = rows * cols / (e2e_s / args.steps) / 1e6
+    clk = clocks.summary()
+    peak = PEAK_FP32_TFLOPS_NOMINAL
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixels/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator of BASELINE.json config 3, SURVEY.md §8d)",
+        "config": dict(config, l2="flushed between steps (256 MiB write)"),
+        "roofline": {"bound": "fp32", "achieved": float(achieved_t.item()), "peak": peak,
+                     "unit": "TFLOP/s", "frac": float(achieved_t.item()) / peak,
+                     "traffic": load_profile_traffic(),
+                     "peak_source": "derived 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (no FP32 "
+                                    "figure in MEASURED_PEAKS.json)",
+                     "kernel": "nlem pixel kernel (+pad), per-step CUDA events",
+                     "algorithmic_flops_per_step": flops,
+                     "frac_at_measured_clock": (float(achieved_t.item()) / peak *
+                                                (clk["sm_max_mhz"] / clk["sm_mhz"])
+                                                if clk.get("sm_mhz") and clk.get("sm_max_mhz")
+                                                else None)},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_val, "unit": "Mpixels/s",
+                "h2d_bytes_per_step": int(band_in.nbytes), "d2h_bytes_per_step": int(nrows * cols * 4),
+                "entry": "nlem_denoise_rows_host (C-ABI, pinned host buffers)"},
+        "clocks": clk,
+        "gpu_launches": 2 * args.steps,
+        "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,514 @@
+// C-ABI layer (include/nlem_b200.h): host-side validation with the reference's
+// messages, buffer management, dispatch to the sm_100a kernels, failure decoding.
+// There is no CPU fallback: every compute entry point runs on the GPU or returns
+// NLEM_CUDA_ERROR.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "launch.h"
+
+namespace nlemk {
+
+const DeviceCaps& device_caps() {
+  static std::mutex mu;
+  static std::vector<DeviceCaps> caps;
+  static std::vector<bool> have;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (static_cast<int>(caps.size()) <= dev) {
+    caps.resize(dev + 1);
+    have.resize(dev + 1, false);
+  }
+  if (!have[dev]) {
+    DeviceCaps c;
+    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&c.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&c.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaDeviceGetAttribute(&c.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&c.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    caps[dev] = c;
+    have[dev] = true;
+  }
+  return caps[dev];
+}
+
+// ---- validation kernels -----------------------------------------------------------
+// code 1: non-finite coordinate, 2: weight non-finite or negative, 3: no positive weight
+__global__ void validate_points_kernel(const float* __restrict__ points,
+                                       const float* __restrict__ weights, int64_t batch, int n,
+                                       int d, unsigned long long* result) {
+  const size_t nd = static_cast<size_t>(n) * d;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    int bad_pt = 0, bad_w = 0, pos = 0;
+    const float* p = points + b * nd;
+    for (size_t i = threadIdx.x; i < nd; i += blockDim.x) bad_pt |= !isfinite(p[i]);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const float w = weights[b * n + k];
+      bad_w |= !(isfinite(w) && w >= 0.0f);
+      pos |= w > 0.0f;
+    }
+    bad_pt = __syncthreads_or(bad_pt);
+    bad_w = __syncthreads_or(bad_w);
+    pos = __syncthreads_or(pos);
+    if (threadIdx.x == 0) {
+      const int code = bad_pt ? 1 : bad_w ? 2 : !pos ? 3 : 0;
+      if (code) atomicMin(result, (static_cast<unsigned long long>(b) << 2) | code);
+    }
+  }
+}
+
+__global__ void validate_image_kernel(const float* __restrict__ img, int64_t count,
+                                      unsigned long long* result) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    bad |= !isfinite(img[i]);
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0 && bad) atomicMin(result, 1ull);
+}
+
+cudaError_t launch_validate_points(const float* points, const float* weights, int64_t batch, int n,
+                                   int d, unsigned long long* result, cudaStream_t stream) {
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batch, device_caps().sms * 8));
+  validate_points_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(points, weights, batch, n,
+                                                                          d, result);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_image(const float* img, int64_t count, unsigned long long* result,
+                                  cudaStream_t stream) {
+  const int64_t grid =
+      std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, device_caps().sms * 8));
+  validate_image_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(img, count, result);
+  return cudaGetLastError();
+}
+
+}  // namespace nlemk
+
+using namespace nlemk;
+
+namespace {
+
+constexpr int kMaxDim = 1024;
+
+nlem_status invalid(nlem_failure* f, const std::string& msg) {
+  if (f) {
+    f->index = -1;
+    f->iteration = 0;
+    f->kind = NLEM_FAIL_NONE;
+    std::snprintf(f->message, sizeof(f->message), "%s", msg.c_str());
+  }
+  return NLEM_INVALID_ARGUMENT;
+}
+
+nlem_status cuda_fail(nlem_failure* f, cudaError_t e) {
+  if (f) {
+    f->index = -1;
+    f->iteration = 0;
+    f->kind = NLEM_FAIL_NONE;
+    std::snprintf(f->message, sizeof(f->message), "CUDA error: %s", cudaGetErrorString(e));
+  }
+  return NLEM_CUDA_ERROR;
+}
+
+void clear(nlem_failure* f) {
+  if (f) {
+    f->index = -1;
+    f->iteration = 0;
+    f->kind = NLEM_FAIL_NONE;
+    f->message[0] = '\0';
+  }
+}
+
+const char* kind_text(int kind) {
+  switch (kind) {
+    case NLEM_FAIL_ADMM_ITERATE: return "non-finite ADMM iterate";
+    case NLEM_FAIL_ADMM_OBJECTIVE: return "non-finite ADMM objective";
+    case NLEM_FAIL_IRLS_ITERATE: return "non-finite IRLS iterate";
+    case NLEM_FAIL_IRLS_OBJECTIVE: return "non-finite IRLS objective";
+    default: return "numeric failure";
+  }
+}
+
+// Decode a FailureSlot; pixel_cols > 0 decorates "pixel (r, c): " (nlem.cpp:60-64).
+nlem_status decode_failure(unsigned long long packed, nlem_failure* f, int64_t pixel_cols) {
+  if (packed == ~0ull) return NLEM_OK;
+  const int64_t index = static_cast<int64_t>(packed >> 24);
+  const int64_t iteration = static_cast<int64_t>((packed >> 4) & 0xFFFFF);
+  const int kind = static_cast<int>(packed & 0xF);
+  if (f) {
+    f->index = index;
+    f->iteration = iteration;
+    f->kind = kind;
+    if (pixel_cols > 0)
+      std::snprintf(f->message, sizeof(f->message), "pixel (%lld, %lld): %s (iteration %lld)",
+                    static_cast<long long>(index / pixel_cols),
+                    static_cast<long long>(index % pixel_cols), kind_text(kind),
+                    static_cast<long long>(iteration));
+    else
+      std::snprintf(f->message, sizeof(f->message), "%s (iteration %lld)", kind_text(kind),
+                    static_cast<long long>(iteration));
+  }
+  return NLEM_NUMERIC_FAILURE;
+}
+
+struct DevSlot {  // one 8-byte device word for a failure/validation record
+  unsigned long long* ptr = nullptr;
+  cudaStream_t stream;
+  explicit DevSlot(cudaStream_t s) : stream(s) {}
+  cudaError_t init() {
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ptr), sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(ptr, 0xFF, sizeof(unsigned long long), stream);
+  }
+  cudaError_t read(unsigned long long* out) {
+    cudaError_t e = cudaMemcpyAsync(out, ptr, sizeof(*out), cudaMemcpyDeviceToHost, stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(stream);
+  }
+  ~DevSlot() {
+    if (ptr) cudaFreeAsync(ptr, stream);
+  }
+};
+
+nlem_status check_box(const nlem_box& box, nlem_failure* f) {
+  if (box.bounded && !(box.lower <= box.upper)) return invalid(f, "box requires lower <= upper");
+  return NLEM_OK;
+}
+
+nlem_status validate_params_impl(const nlem_params* p, nlem_failure* f) {
+  if (p == nullptr) return invalid(f, "params must not be null");
+  // proj/src/nlm.cpp:17-29, same order and messages
+  if (p->search < 1 || p->search % 2 == 0) return invalid(f, "search window must be odd and positive");
+  if (p->patch < 1 || p->patch % 2 == 0) return invalid(f, "patch size must be odd and positive");
+  if (p->patch > p->search) return invalid(f, "patch size must not exceed the search window");
+  if (!(p->h > 0.0f)) return invalid(f, "similarity bandwidth h must be positive");
+  if (!(p->sigma >= 0.0f)) return invalid(f, "sigma must be nonnegative");
+  if (p->solver_iters < 1) return invalid(f, "solver_iters must be at least 1");
+  if (!(p->mu > 0.0f)) return invalid(f, "penalty mu must be positive");
+  if (!(p->epsilon > 0.0f)) return invalid(f, "epsilon must be positive");
+  if (p->solver < 0 || p->solver > 2) return invalid(f, "unknown solver");
+  if (p->init_mode < 0 || p->init_mode > 1) return invalid(f, "unknown init mode");
+  if (p->patch * p->patch > kMaxDim) return invalid(f, "patch dimension k*k above 1024 is not supported");
+  return check_box(p->range, f);
+}
+
+nlem_status validate_points_dev(const float* points, const float* weights, int64_t batch, int n,
+                                int d, nlem_failure* f, cudaStream_t s) {
+  DevSlot slot(s);
+  cudaError_t e = slot.init();
+  if (e == cudaSuccess) e = launch_validate_points(points, weights, batch, n, d, slot.ptr, s);
+  unsigned long long v = ~0ull;
+  if (e == cudaSuccess) e = slot.read(&v);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  if (v == ~0ull) return NLEM_OK;
+  const int code = static_cast<int>(v & 3);
+  // types.hpp:58-68 messages
+  const char* msg = code == 1 ? "point coordinates must be finite"
+                    : code == 2 ? "weights must be finite and nonnegative"
+                                : "at least one weight must be positive";
+  nlem_status st = invalid(f, msg);
+  if (f) f->index = static_cast<int64_t>(v >> 2);
+  return st;
+}
+
+int res_mode_for(float tol, bool trace_res) {
+  if (trace_res || tol > 0.0f) return RES_FULL;
+  if (tol == 0.0f) return RES_EXACT0;
+  return RES_NONE;
+}
+
+NlemDevParams dev_params(const nlem_params& p) {
+  NlemDevParams d;
+  d.search = p.search;
+  d.patch = p.patch;
+  const double h = static_cast<double>(p.h);
+  d.inv_h2 = static_cast<float>(1.0 / (h * h));
+  d.solver = p.solver;
+  d.iters = p.solver_iters;
+  d.mu = p.mu;
+  d.epsilon = p.epsilon;
+  d.init_mode = p.init_mode;
+  d.range = p.range;
+  d.irls_tol = p.irls_tol;
+  return d;
+}
+
+int64_t mirror_host(int64_t i, int64_t n) {
+  if (n == 1) return 0;
+  const int64_t period = 2 * (n - 1);
+  int64_t m = i % period;
+  if (m < 0) m += period;
+  return m < n ? m : period - m;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nlem_version(void) { return "nlem_b200 0.1 (sm_100a)"; }
+
+const char* nlem_status_string(nlem_status s) {
+  switch (s) {
+    case NLEM_OK: return "ok";
+    case NLEM_INVALID_ARGUMENT: return "invalid argument";
+    case NLEM_NUMERIC_FAILURE: return "numeric failure";
+    case NLEM_CUDA_ERROR: return "CUDA error";
+  }
+  return "unknown";
+}
+
+nlem_status nlem_validate_params(const nlem_params* params, nlem_failure* failure) {
+  clear(failure);
+  return validate_params_impl(params, failure);
+}
+
+int32_t nlem_default_init_mode(float sigma) {  // proj/src/nlm.cpp:13-15
+  return sigma <= 60.0f ? NLEM_INIT_NOISY_PATCH : NLEM_INIT_NLM_PATCH;
+}
+
+int64_t nlem_band_halo(const nlem_params* p) { return p->search / 2 + p->patch / 2; }
+
+nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t batch, int64_t n,
+                              int64_t d, const float* z_init, nlem_box box, nlem_admm_config cfg,
+                              float* z_out, float* objective_out, int32_t* iters_out,
+                              float* trace_objective, float* trace_residual, nlem_failure* failure,
+                              void* stream) {
+  clear(failure);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (batch < 0) return invalid(failure, "batch must be nonnegative");
+  if (n < 1) return invalid(failure, "point set must contain at least one point");
+  if (d < 1 || d > kMaxDim) return invalid(failure, "point dimension must be in [1, 1024]");
+  if (!(cfg.mu > 0.0f)) return invalid(failure, "penalty mu must be positive");  // admm.hpp:30-34
+  if (cfg.max_iter < 1) return invalid(failure, "max_iter must be at least 1");
+  if (nlem_status st = check_box(box, failure)) return st;
+  if (batch == 0) return NLEM_OK;
+  if (!points || !weights || !z_out) return invalid(failure, "null buffer");
+  if (n * d > (int64_t(1) << 31)) return invalid(failure, "point set too large");
+  if (failure) {
+    if (nlem_status st = validate_points_dev(points, weights, batch, static_cast<int>(n),
+                                             static_cast<int>(d), failure, s))
+      return st;
+  }
+  DevSlot slot(s);
+  cudaError_t e = slot.init();
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  AdmmLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), z_init, box,
+               cfg.mu, cfg.max_iter, cfg.tol_primal,
+               res_mode_for(cfg.tol_primal, trace_residual != nullptr), z_out, objective_out,
+               iters_out, trace_objective, trace_residual, reinterpret_cast<FailureSlot*>(slot.ptr)};
+  e = admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  if (!failure) return NLEM_OK;
+  unsigned long long v = ~0ull;
+  if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
+  return decode_failure(v, failure, 0);
+}
+
+nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t batch, int64_t n,
+                              int64_t d, const float* x_init, nlem_irls_config cfg, float* x_out,
+                              float* objective_out, int32_t* iters_out, float* trace_objective,
+                              nlem_failure* failure, void* stream) {
+  clear(failure);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (batch < 0) return invalid(failure, "batch must be nonnegative");
+  if (n < 1) return invalid(failure, "point set must contain at least one point");
+  if (d < 1 || d > kMaxDim) return invalid(failure, "point dimension must be in [1, 1024]");
+  if (!(cfg.epsilon > 0.0f)) return invalid(failure, "epsilon must be positive");  // irls.hpp:24-28
+  if (cfg.max_iter < 1) return invalid(failure, "max_iter must be at least 1");
+  if (batch == 0) return NLEM_OK;
+  if (!points || !weights || !x_out) return invalid(failure, "null buffer");
+  if (failure) {
+    if (nlem_status st = validate_points_dev(points, weights, batch, static_cast<int>(n),
+                                             static_cast<int>(d), failure, s))
+      return st;
+  }
+  DevSlot slot(s);
+  cudaError_t e = slot.init();
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  IrlsLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), x_init,
+               cfg.epsilon, cfg.max_iter, cfg.tol, x_out, objective_out, iters_out,
+               trace_objective, reinterpret_cast<FailureSlot*>(slot.ptr)};
+  e = launch_irls_generic(L, s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  if (!failure) return NLEM_OK;
+  unsigned long long v = ~0ull;
+  if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
+  return decode_failure(v, failure, 0);
+}
+
+nlem_status nlem_denoise_rows(const float* noisy, int64_t in_row0, int64_t in_rows, int64_t rows,
+                              int64_t cols, int64_t out_row0, int64_t out_rows,
+                              const nlem_params* params, float* out, float* frames,
+                              nlem_failure* failure, void* stream) {
+  clear(failure);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (rows < 1 || cols < 1) return invalid(failure, "image must be non-empty");  // image.hpp:15
+  if (nlem_status st = validate_params_impl(params, failure)) return st;
+  if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > rows)
+    return invalid(failure, "output rows outside the image");
+  if (in_row0 < 0 || in_rows < 1 || in_row0 + in_rows > rows)
+    return invalid(failure, "input rows outside the image");
+  if (out_rows == 0) return NLEM_OK;
+  if (!noisy || !out) return invalid(failure, "null buffer");
+  const int hs = params->search / 2, hk = params->patch / 2;
+  const int64_t win_r0 = std::max<int64_t>(0, out_row0 - hs);
+  const int64_t win_r1 = std::min<int64_t>(rows, out_row0 + out_rows + hs);
+  const int64_t pad_row0 = win_r0 - hk;
+  const int64_t pad_rows = (win_r1 - win_r0) + 2 * hk;
+  const int64_t pad_cols = cols + 2 * hk;
+  for (int64_t r = pad_row0; r < pad_row0 + pad_rows; ++r) {
+    const int64_t g = mirror_host(r, rows);
+    if (g < in_row0 || g >= in_row0 + in_rows)
+      return invalid(failure, "input rows do not cover the band and its halo");
+  }
+  if (failure) {  // image.hpp:16 over the rows this band reads
+    DevSlot vs(s);
+    cudaError_t e = vs.init();
+    if (e == cudaSuccess) e = launch_validate_image(noisy, in_rows * cols, vs.ptr, s);
+    unsigned long long v = ~0ull;
+    if (e == cudaSuccess) e = vs.read(&v);
+    if (e != cudaSuccess) return cuda_fail(failure, e);
+    if (v != ~0ull) return invalid(failure, "image intensities must be finite");
+  }
+  float* pad = nullptr;
+  cudaError_t e = cudaMallocAsync(&pad, pad_rows * pad_cols * sizeof(float), s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  DevSlot slot(s);
+  e = slot.init();
+  if (e == cudaSuccess)
+    e = launch_pad_band(noisy, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hk, s);
+  if (e == cudaSuccess) {
+    NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
+                 dev_params(*params), out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
+    e = nlem_fast_supported(L) ? launch_nlem_fast(L, s) : launch_nlem_generic(L, s);
+  }
+  cudaFreeAsync(pad, s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  if (!failure) return NLEM_OK;
+  unsigned long long v = ~0ull;
+  if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
+  return decode_failure(v, failure, cols);
+}
+
+nlem_status nlem_denoise(const float* noisy, int64_t rows, int64_t cols, const nlem_params* params,
+                         float* out, float* frames, nlem_failure* failure, void* stream) {
+  return nlem_denoise_rows(noisy, 0, rows, rows, cols, 0, rows, params, out, frames, failure,
+                           stream);
+}
+
+nlem_status nlm_denoise(const float* noisy, int64_t rows, int64_t cols, const nlem_params* params,
+                        float* out, nlem_failure* failure, void* stream) {
+  if (params == nullptr) return invalid(failure, "params must not be null");
+  nlem_params p = *params;
+  p.solver = NLEM_SOLVER_NLM_ONLY;  // centre of the weighted-mean patch (test_denoise.cpp:228-240)
+  return nlem_denoise_rows(noisy, 0, rows, rows, cols, 0, rows, &p, out, nullptr, failure, stream);
+}
+
+nlem_status nlem_admm_batched_host(const float* points, const float* weights, int64_t batch,
+                                   int64_t n, int64_t d, const float* z_init, nlem_box box,
+                                   nlem_admm_config cfg, float* z_out, float* objective_out,
+                                   int32_t* iters_out, float* trace_objective,
+                                   float* trace_residual, nlem_failure* failure, int32_t device) {
+  nlem_failure local;
+  nlem_failure* f = failure ? failure : &local;
+  clear(f);
+  if (batch <= 0 || n < 1 || d < 1)
+    return nlem_admm_batched(nullptr, nullptr, batch, n, d, nullptr, box, cfg, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, f, nullptr);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t P = static_cast<size_t>(batch) * n * d, Wn = static_cast<size_t>(batch) * n,
+               Z = static_cast<size_t>(batch) * d, Tn = static_cast<size_t>(batch) * cfg.max_iter;
+  float *dp = nullptr, *dw = nullptr, *dzi = nullptr, *dz = nullptr, *dob = nullptr, *dto = nullptr,
+        *dtr = nullptr;
+  int32_t* dit = nullptr;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMallocAsync(p, bytes, s);
+  };
+  alloc(reinterpret_cast<void**>(&dp), P * 4);
+  alloc(reinterpret_cast<void**>(&dw), Wn * 4);
+  alloc(reinterpret_cast<void**>(&dz), Z * 4);
+  if (z_init) alloc(reinterpret_cast<void**>(&dzi), Z * 4);
+  if (objective_out) alloc(reinterpret_cast<void**>(&dob), batch * 4);
+  if (iters_out) alloc(reinterpret_cast<void**>(&dit), batch * 4);
+  if (trace_objective) alloc(reinterpret_cast<void**>(&dto), Tn * 4);
+  if (trace_residual) alloc(reinterpret_cast<void**>(&dtr), Tn * 4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, points, P * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, weights, Wn * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && dzi) e = cudaMemcpyAsync(dzi, z_init, Z * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && dto) e = cudaMemcpyAsync(dto, trace_objective, Tn * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(dtr, trace_residual, Tn * 4, cudaMemcpyHostToDevice, s);
+  nlem_status st = NLEM_OK;
+  if (e == cudaSuccess)
+    st = nlem_admm_batched(dp, dw, batch, n, d, dzi, box, cfg, dz, dob, dit, dto, dtr, f, s);
+  if (e == cudaSuccess && st == NLEM_OK) {
+    e = cudaMemcpyAsync(z_out, dz, Z * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dob) e = cudaMemcpyAsync(objective_out, dob, batch * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dit) e = cudaMemcpyAsync(iters_out, dit, batch * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dto) e = cudaMemcpyAsync(trace_objective, dto, Tn * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dtr) e = cudaMemcpyAsync(trace_residual, dtr, Tn * 4, cudaMemcpyDeviceToHost, s);
+  }
+  for (void* p : {static_cast<void*>(dp), static_cast<void*>(dw), static_cast<void*>(dzi),
+                  static_cast<void*>(dz), static_cast<void*>(dob), static_cast<void*>(dit),
+                  static_cast<void*>(dto), static_cast<void*>(dtr)})
+    if (p) cudaFreeAsync(p, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  return st;
+}
+
+nlem_status nlem_denoise_rows_host(const float* noisy, int64_t in_row0, int64_t in_rows,
+                                   int64_t rows, int64_t cols, int64_t out_row0, int64_t out_rows,
+                                   const nlem_params* params, float* out, float* frames,
+                                   nlem_failure* failure, int32_t device) {
+  nlem_failure local;
+  nlem_failure* f = failure ? failure : &local;
+  clear(f);
+  if (rows < 1 || cols < 1) return invalid(f, "image must be non-empty");
+  if (nlem_status st = validate_params_impl(params, f)) return st;
+  if (in_rows < 1 || out_rows < 0) return invalid(f, "row range outside the image");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t in_px = static_cast<size_t>(in_rows) * cols;
+  const size_t out_px = static_cast<size_t>(out_rows) * cols;
+  const size_t fr = frames ? out_px * params->solver_iters : 0;
+  float *din = nullptr, *dout = nullptr, *dfr = nullptr;
+  e = cudaMallocAsync(&din, in_px * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dout, std::max<size_t>(out_px, 1) * 4, s);
+  if (e == cudaSuccess && frames) e = cudaMallocAsync(&dfr, std::max<size_t>(fr, 1) * 4, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(din, noisy, in_px * 4, cudaMemcpyHostToDevice, s);
+  nlem_status st = NLEM_OK;
+  if (e == cudaSuccess)
+    st = nlem_denoise_rows(din, in_row0, in_rows, rows, cols, out_row0, out_rows, params, dout, dfr,
+                           f, s);
+  if (e == cudaSuccess && st == NLEM_OK && out_px) {
+    e = cudaMemcpyAsync(out, dout, out_px * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && frames) e = cudaMemcpyAsync(frames, dfr, fr * 4, cudaMemcpyDeviceToHost, s);
+  }
+  if (din) cudaFreeAsync(din, s);
+  if (dout) cudaFreeAsync(dout, s);
+  if (dfr) cudaFreeAsync(dfr, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  return st;
+}
+
+nlem_status nlem_denoise_host(const float* noisy, int64_t rows, int64_t cols,
+                              const nlem_params* params, float* out, float* frames,
+                              nlem_failure* failure, int32_t device) {
+  return nlem_denoise_rows_host(noisy, 0, rows, rows, cols, 0, rows, params, out, frames, failure,
+                                device);
+}
+
+}  // extern "C"

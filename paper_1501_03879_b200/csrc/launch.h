@@ -1,0 +1,97 @@
+// Internal host-side launch descriptors shared by the C-ABI layer and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/nlem_b200.h"
+#include "common.cuh"
+
+namespace nlemk {
+
+struct DeviceCaps {
+  int sms = 148;
+  int max_smem_optin = 232448;  // per-CTA opt-in limit
+  int smem_per_sm = 233472;
+  int cc_major = 10, cc_minor = 0;
+};
+
+const DeviceCaps& device_caps();  // of the current device (cached per device)
+
+struct AdmmLaunch {
+  const float* points;
+  const float* weights;
+  int64_t batch;
+  int n, d;
+  const float* z_init;
+  nlem_box box;
+  float mu;
+  int max_iter;
+  float tol;
+  int res_mode;
+  float* z_out;
+  float* obj_out;
+  int* iters_out;
+  float* tr_obj;
+  float* tr_res;
+  FailureSlot* fail;
+};
+
+struct IrlsLaunch {
+  const float* points;
+  const float* weights;
+  int64_t batch;
+  int n, d;
+  const float* x_init;
+  float eps;
+  int max_iter;
+  float tol;
+  float* x_out;
+  float* obj_out;
+  int* iters_out;
+  float* tr_obj;
+  FailureSlot* fail;
+};
+
+struct NlemDevParams {
+  int search, patch;
+  float inv_h2;  // 1 / h^2 (patch.cpp:56)
+  int solver, iters;
+  float mu, epsilon;
+  int init_mode;
+  nlem_box range;
+  float irls_tol;
+};
+
+struct NlemLaunch {
+  const float* pad;  // mirror-padded band, row 0 = global row pad_row0, col 0 = global col -k/2
+  int64_t pad_row0, pad_rows, pad_cols;
+  int64_t rows, cols;          // full image
+  int64_t out_row0, out_rows;  // output band
+  NlemDevParams P;
+  float* out;     // [out_rows][cols]
+  float* frames;  // [iters][out_rows][cols] or null
+  FailureSlot* fail;
+};
+
+cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream);
+cudaError_t launch_irls_generic(const IrlsLaunch& L, cudaStream_t stream);
+cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t rows, int64_t cols,
+                            float* pad, int64_t pad_row0, int64_t pad_rows, int64_t pad_cols, int hk,
+                            cudaStream_t stream);
+cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream);
+
+// Specialised register-tiled kernels (kernels_fast.cu).  Return false when the
+// shape is not covered (the caller then uses the generic kernel).
+bool admm_fast_supported(const AdmmLaunch& L);
+cudaError_t launch_admm_fast(const AdmmLaunch& L, cudaStream_t stream);
+bool nlem_fast_supported(const NlemLaunch& L);
+cudaError_t launch_nlem_fast(const NlemLaunch& L, cudaStream_t stream);
+
+// validation kernels (types.hpp:58-68, image.hpp:14-17): packed (index << 2 | code), ~0 = ok
+cudaError_t launch_validate_points(const float* points, const float* weights, int64_t batch,
+                                   int n, int d, unsigned long long* result, cudaStream_t stream);
+cudaError_t launch_validate_image(const float* img, int64_t count, unsigned long long* result,
+                                  cudaStream_t stream);
+
+}  // namespace nlemk

@@ -1,0 +1,288 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the FP64 oracle and
+the reference's known-answer tests.  Bar (BASELINE.json north_star): max |GPU -
+oracle| <= 1e-2 gray levels, |dPSNR| <= 0.01 dB, identical iteration counts."""
+import numpy as np
+import pytest
+
+from tests.support import house_like, kats, random_instance
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2      # gray levels (north_star)
+PSNR_TOL = 0.01  # dB
+
+K = kats()
+
+
+@pytest.fixture(scope="module")
+def nb():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1501_03879_b200 as nb
+
+    return nb
+
+
+def _solve(nb, k, trace=False):
+    cfg = nb.AdmmConfig(mu=k["mu"], max_iter=k["max_iter"], tol_primal=k.get("tol_primal", 0.0),
+                        z_init=k.get("z_init"), record_trace=trace)
+    return nb.admm_euclidean_median(np.array(k["points"], np.float32),
+                                    np.array(k["weights"], np.float32),
+                                    nb.BoxConstraint.unconstrained(), cfg)
+
+
+# ---------------------------------------------------------------- reference KATs on GPU
+def test_admm_single_point_kats(nb):
+    r = _solve(nb, K["admm_single_point_distant_start"])
+    assert r.iterations_run == 1 and np.linalg.norm(r.minimizer) == 0.0 and r.objective == 0.0
+    r = _solve(nb, K["admm_single_point_undersized_radius"])
+    assert r.iterations_run == 1 and r.objective == pytest.approx(3.0, rel=1e-6)
+    k = K["admm_single_point_default_start"]
+    r = _solve(nb, k)
+    assert r.minimizer.tolist() == k["expected_minimizer"] and r.objective == 0.0
+
+
+def test_admm_recursion_kat(nb):
+    k = K["admm_recursion"]
+    r = _solve(nb, k, trace=True)
+    assert [t.objective for t in r.trace[:2]] == k["expected_trace_objective"]
+    assert [t.primal_residual for t in r.trace[:2]] == k["expected_trace_residual"]
+    assert r.trace[2].primal_residual <= 1e-6
+    assert r.minimizer[0] == pytest.approx(0.5, rel=1e-6)
+    assert r.objective == pytest.approx(1.0, rel=1e-6)
+
+
+def test_admm_triangle_kat(nb):
+    k = K["admm_equilateral_triangle"]
+    k = dict(k, max_iter=20000)
+    r = _solve(nb, k)
+    np.testing.assert_allclose(r.minimizer, k["expected_minimizer"], rtol=1e-5)
+    assert r.objective == pytest.approx(k["expected_objective"], rel=1e-6)
+
+
+def test_irls_kats(nb):
+    k = K["irls_single_point"]
+    r = nb.irls_euclidean_median(np.array(k["points"], np.float32), np.ones(1, np.float32),
+                                 nb.IrlsConfig(epsilon=1e-6, max_iter=1))
+    assert np.abs(r.minimizer - 2.5).max() <= 1e-6 and r.iterations_run == 1
+    k = K["irls_equilateral_corner_start"]
+    r = nb.irls_euclidean_median(np.array(k["points"], np.float32), np.ones(3, np.float32),
+                                 nb.IrlsConfig(epsilon=1e-6, max_iter=2000, x_init=[0.0, 0.0]))
+    np.testing.assert_allclose(r.minimizer, k["expected_minimizer"], rtol=1e-4)
+
+
+def test_overflow_raises_numeric_failure(nb):  # test_solvers.cpp:342-368 (float range)
+    pts = np.array([[0.0, 0.0], [10.0, 0.0]], np.float32)
+    w = np.array([3e38, 3e38], np.float32)
+    with pytest.raises(nb.NumericFailure) as e:
+        nb.admm_euclidean_median(pts, w, None, nb.AdmmConfig(mu=1.0, max_iter=5, record_trace=True))
+    assert e.value.iteration >= 1 and "objective" in str(e.value)
+    with pytest.raises(nb.NumericFailure):
+        nb.irls_euclidean_median(pts, w, nb.IrlsConfig(max_iter=5))
+
+
+def test_solver_validation(nb):  # test_solvers.cpp:370-395
+    pts = np.zeros((1, 2), np.float32)
+    w = np.ones(1, np.float32)
+    with pytest.raises(nb.InvalidArgument, match="penalty mu must be positive"):
+        nb.admm_euclidean_median(pts, w, None, nb.AdmmConfig(mu=0.0))
+    with pytest.raises(nb.InvalidArgument, match="z_init dimension"):
+        nb.admm_euclidean_median(pts, w, None, nb.AdmmConfig(z_init=np.zeros(3)))
+    with pytest.raises(nb.InvalidArgument, match="epsilon must be positive"):
+        nb.irls_euclidean_median(pts, w, nb.IrlsConfig(epsilon=0.0))
+    with pytest.raises(nb.InvalidArgument, match="at least one point"):
+        nb.admm_euclidean_median(np.zeros((1, 0, 2), np.float32), np.zeros((1, 0), np.float32))
+    with pytest.raises(nb.InvalidArgument, match="finite and nonnegative"):
+        nb.admm_euclidean_median(pts, -w)
+    with pytest.raises(nb.InvalidArgument, match="at least one weight must be positive"):
+        nb.admm_euclidean_median(pts, 0 * w)
+    with pytest.raises(nb.InvalidArgument, match="coordinates must be finite"):
+        nb.admm_euclidean_median(pts + np.inf, w)
+
+
+def _small(nb, solver, **kw):  # test_denoise.cpp:74-84
+    base = dict(search=7, patch=3, h=30.0, sigma=15.0, solver=solver, solver_iters=4)
+    base.update(kw)
+    return nb.NlemParams(**base)
+
+
+def test_constant_image_fixed_point(nb):  # test_denoise.cpp:165-179
+    img = np.full((12, 10), 77.0, np.float32)
+    assert (nb.nlem_denoise(img, _small(nb, "admm")) == 77.0).all()
+    assert (nb.nlem_denoise(img, _small(nb, "admm", init_mode="nlm")) == 77.0).all()
+    assert (nb.nlm_denoise(img, _small(nb, "admm")) == 77.0).all()
+    assert np.abs(nb.nlem_denoise(img, _small(nb, "irls")) - 77.0).max() <= 1e-4
+    assert np.abs(nb.nlem_denoise(img, _small(nb, "nlm_only")) - 77.0).max() <= 1e-4
+
+
+def test_snapshots_forward_fill(nb):  # test_denoise.cpp:282-290
+    img = np.full((8, 8), 50.0, np.float32)
+    frames = nb.nlem_denoise_snapshots(img, _small(nb, "admm", solver_iters=4))
+    assert frames.shape == (4, 8, 8) and (frames == 50.0).all()
+
+
+def test_vanishing_bandwidth_identity(nb):  # test_denoise.cpp:195-212
+    img = np.round(house_like(12)).astype(np.float32)
+    assert (nb.nlm_denoise(img, _small(nb, "admm", h=1e-6)) == img).all()
+    assert np.abs(nb.nlem_denoise(img, _small(nb, "admm", h=1e-6)) - img).max() <= 1e-4
+    assert np.abs(nb.nlem_denoise(img, _small(nb, "irls", h=1e-6)) - img).max() <= 1e-4
+
+
+def test_box_prior(nb, oracle):  # test_denoise.cpp:214-226
+    noisy = oracle.add_gaussian_noise(house_like(12), 25.0, 9).astype(np.float32)
+    for s in ("admm", "irls", "nlm_only"):
+        out = nb.nlem_denoise(noisy, _small(nb, s, range=nb.BoxConstraint.interval(100.0, 140.0)))
+        assert out.min() >= 100.0 and out.max() <= 140.0
+
+
+def test_snapshot_equals_truncated_run_bitwise(nb, oracle):  # test_denoise.cpp:264-280
+    noisy = oracle.add_gaussian_noise(house_like(10), 20.0, 11).astype(np.float32)
+    for s in ("admm", "irls"):
+        frames = nb.nlem_denoise_snapshots(noisy, _small(nb, s, solver_iters=3))
+        for t in (1, 2, 3):
+            direct = nb.nlem_denoise(noisy, _small(nb, s, solver_iters=t))
+            assert (frames[t - 1] == direct).all()
+
+
+def test_failure_carries_pixel(nb):  # test_denoise.cpp:323-338 (1e30: float range)
+    img = np.fromfunction(lambda r, c: np.where((r + c) % 2 == 0, 0.0, 1e30), (8, 8)).astype(np.float32)
+    with pytest.raises(nb.NumericFailure) as e:
+        nb.nlem_denoise(img, _small(nb, "irls", range=nb.BoxConstraint.unconstrained()))
+    assert "pixel (" in str(e.value)
+    with pytest.raises(nb.InvalidArgument, match="intensities must be finite"):
+        nb.nlem_denoise(np.full((4, 4), np.inf, np.float32), _small(nb, "admm"))
+
+
+def test_patchwise_mean_equals_nlm(nb, oracle):  # test_denoise.cpp:228-240
+    noisy = oracle.add_gaussian_noise(house_like(12), 18.0, 6).astype(np.float32)
+    a = nb.nlem_denoise(noisy, _small(nb, "nlm_only"))
+    b = nb.nlm_denoise(noisy, _small(nb, "nlm_only"))
+    np.testing.assert_allclose(a, b, rtol=1e-6)
+
+
+# ---------------------------------------------------------------- oracle parity
+def _params_pair(nb, oracle, *, search, patch, h, iters, solver="admm", init="nlm", mu=1.0,
+                 eps=1e-6, irls_tol=0.0, box=(0.0, 255.0)):
+    g = nb.NlemParams(search=search, patch=patch, h=h, solver=solver, solver_iters=iters, mu=mu,
+                      epsilon=eps, init_mode=init, irls_tol=irls_tol,
+                      range=nb.BoxConstraint.interval(*box) if box else nb.BoxConstraint.unconstrained())
+    o = oracle.make_params(search=search, patch=patch, h=h, solver={"nlm_only": "nlm"}.get(solver, solver),
+                           solver_iters=iters, mu=mu, epsilon=eps, init_mode=init, box=box,
+                           irls_tol=irls_tol)
+    return g, o
+
+
+def test_config0_full_image_parity(nb, oracle):
+    """BASELINE config 0: 128^2, k=5, S=11, h=10*sigma (d*h^2 -> h_ref = h*sqrt(d)), T=20."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(0)
+    g, o = _params_pair(nb, oracle, search=11, patch=5, h=synth.reference_h(20.0, 25), iters=20)
+    gpu = nb.nlem_denoise(noisy, g)
+    ref = oracle.nlem_denoise(noisy.astype(np.float64), o)
+    assert np.abs(gpu - ref).max() <= TOL
+    assert abs(oracle.psnr(clean, gpu) - oracle.psnr(clean, ref)) <= PSNR_TOL
+
+
+def test_config1_subset_parity(nb, oracle):
+    """BASELINE config 1 (first 192 problems, n=441, d=49, T=50, mu=1), box and unconstrained."""
+    from paper_1501_03879_b200 import synth
+
+    pts, w = synth.point_sets(192)
+    for box in (nb.BoxConstraint.interval(0.0, 255.0), nb.BoxConstraint.unconstrained()):
+        r = nb.admm_euclidean_median(pts, w, box, nb.AdmmConfig(mu=1.0, max_iter=50))
+        ref = oracle.admm_batched(pts.astype(np.float64), w.astype(np.float64), mu=1.0, max_iter=50,
+                                  box=(0.0, 255.0) if box.is_bounded() else None)
+        assert np.abs(r.minimizer - ref.minimizer).max() <= TOL
+        np.testing.assert_allclose(r.objective, ref.objective, rtol=1e-5)
+        assert (r.iterations_run == ref.iterations).all()
+
+
+def test_config2_band_parity(nb, oracle):
+    """BASELINE config 2 generator (512^2, k=7, S=21, T=10) on two 6-row bands (top edge and
+    interior) through the row-band entry point, global coordinates."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(2)
+    g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(20.0, 49), iters=10)
+    import torch
+
+    X = torch.from_numpy(noisy).cuda()
+    for r0 in (0, 250, 506):
+        gpu = nb.nlem_denoise_rows(X, 0, 512, 512, r0, 6, g).cpu().numpy()
+        ref = oracle.nlem_denoise(noisy.astype(np.float64), o, rows=(r0, r0 + 6))[r0:r0 + 6]
+        assert np.abs(gpu - ref).max() <= TOL
+
+
+@pytest.mark.parametrize("sigma", [10.0, 40.0])
+def test_config4_snapshot_sweep_parity(nb, oracle, sigma):
+    """Config-4 style sweep on a 48^2 crop: ADMM and IRLS (eps=1e-4, tol<0) T=1..60,
+    PSNR vs clean at every iteration within 0.01 dB of the oracle."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(48, 48, 6, 4, sigma)
+    for solver, kw in (("admm", {}), ("irls", dict(eps=1e-4, irls_tol=-1.0))):
+        g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(sigma, 49),
+                            iters=60, solver=solver, **kw)
+        fg = nb.nlem_denoise_snapshots(noisy, g)
+        _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
+        assert np.abs(fg - fo).max() <= TOL
+        for t in range(60):
+            assert abs(oracle.psnr(clean, fg[t]) - oracle.psnr(clean, fo[t])) <= PSNR_TOL
+
+
+@pytest.mark.parametrize("n,d,box", [(2, 1, None), (3, 2, (0.4, 0.6)), (37, 5, None),
+                                     (120, 33, (0.2, 0.8)), (60, 70, None), (4000, 16, None),
+                                     (300, 130, (0.0, 1.0))])
+def test_random_instances_vs_oracle(nb, oracle, n, d, box):
+    rng = np.random.default_rng(n * 1000 + d)
+    B = 6
+    pts = rng.uniform(0, 1, size=(B, n, d)).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, size=(B, n)).astype(np.float32)
+    nbox = nb.BoxConstraint.interval(*box) if box else nb.BoxConstraint.unconstrained()
+    for tol, trace in ((0.0, False), (1e-3, True), (-1.0, False)):
+        r = nb.admm_euclidean_median(pts, w, nbox, nb.AdmmConfig(mu=2.0, max_iter=40, tol_primal=tol,
+                                                                 record_trace=trace))
+        ref = oracle.admm_batched(pts.astype(np.float64), w.astype(np.float64), mu=2.0, max_iter=40,
+                                  tol_primal=tol, box=box, trace=trace)
+        assert np.abs(r.minimizer - ref.minimizer).max() <= 1e-4
+        if trace:
+            for b in range(B):
+                to = np.array([t.objective for t in r.trace[b]])
+                tr = np.array([t.primal_residual for t in r.trace[b]])
+                np.testing.assert_allclose(to, ref.trace_objective[b, :len(to)], rtol=1e-4)
+                np.testing.assert_allclose(tr, ref.trace_residual[b, :len(tr)], rtol=2e-2, atol=1e-5)
+        ir = nb.irls_euclidean_median(pts, w, nb.IrlsConfig(epsilon=1e-4, max_iter=30, tol=-1.0))
+        iref = oracle.irls_batched(pts.astype(np.float64), w.astype(np.float64), epsilon=1e-4,
+                                   max_iter=30, tol=-1.0)
+        assert np.abs(ir.minimizer - iref.minimizer).max() <= 1e-4
+
+
+def test_determinism_and_band_invariance(nb):
+    """Bitwise reruns, and bitwise equality of 1 band vs 3 bands (the multi-GPU split)."""
+    import torch
+
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(96, 80, 10, 6, 20.0)
+    p = nb.NlemParams(search=21, patch=7, h=synth.reference_h(20.0, 49), solver_iters=10, mu=1.0,
+                      init_mode="nlm")
+    a = nb.nlem_denoise(noisy, p)
+    b = nb.nlem_denoise(noisy, p)
+    assert (a == b).all()
+    X = torch.from_numpy(noisy).cuda()
+    halo = nb.band_halo(p)
+    parts = []
+    for r0, r1 in ((0, 30), (30, 61), (61, 96)):
+        i0, i1 = max(0, r0 - halo), min(96, r1 + halo)
+        parts.append(nb.nlem_denoise_rows(X[i0:i1], i0, 96, 80, r0, r1 - r0, p).cpu().numpy())
+    assert (np.concatenate(parts) == a).all()
+
+
+def test_host_entry_matches_device(nb):
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(64, 64, 8, 5, 20.0)
+    p = nb.NlemParams(search=11, patch=5, h=synth.reference_h(20.0, 25), solver_iters=5, mu=1.0)
+    assert (nb.nlem_denoise_host(noisy, p) == nb.nlem_denoise(noisy, p)).all()
