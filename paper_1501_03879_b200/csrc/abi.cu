@@ -237,6 +237,7 @@ NlemDevParams dev_params(const nlem_params& p) {
   d.init_mode = p.init_mode;
   d.range = p.range;
   d.irls_tol = p.irls_tol;
+  d.nlm_ratio = 0;
   return d;
 }
 
@@ -343,10 +344,14 @@ nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t
   return decode_failure(v, failure, 0);
 }
 
-nlem_status nlem_denoise_rows(const float* noisy, int64_t in_row0, int64_t in_rows, int64_t rows,
+}  // extern "C"
+
+namespace {
+
+nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_rows, int64_t rows,
                               int64_t cols, int64_t out_row0, int64_t out_rows,
                               const nlem_params* params, float* out, float* frames,
-                              nlem_failure* failure, void* stream) {
+                              nlem_failure* failure, void* stream, int nlm_ratio) {
   clear(failure);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows < 1 || cols < 1) return invalid(failure, "image must be non-empty");  // image.hpp:15
@@ -385,8 +390,10 @@ nlem_status nlem_denoise_rows(const float* noisy, int64_t in_row0, int64_t in_ro
   if (e == cudaSuccess)
     e = launch_pad_band(noisy, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hk, s);
   if (e == cudaSuccess) {
+    NlemDevParams dp = dev_params(*params);
+    dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
-                 dev_params(*params), out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
+                 dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
     e = nlem_fast_supported(L) ? launch_nlem_fast(L, s) : launch_nlem_generic(L, s);
   }
   cudaFreeAsync(pad, s);
@@ -395,6 +402,18 @@ nlem_status nlem_denoise_rows(const float* noisy, int64_t in_row0, int64_t in_ro
   unsigned long long v = ~0ull;
   if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
   return decode_failure(v, failure, cols);
+}
+
+}  // namespace
+
+extern "C" {
+
+nlem_status nlem_denoise_rows(const float* noisy, int64_t in_row0, int64_t in_rows, int64_t rows,
+                              int64_t cols, int64_t out_row0, int64_t out_rows,
+                              const nlem_params* params, float* out, float* frames,
+                              nlem_failure* failure, void* stream) {
+  return denoise_rows_impl(noisy, in_row0, in_rows, rows, cols, out_row0, out_rows, params, out,
+                           frames, failure, stream, 0);
 }
 
 nlem_status nlem_denoise(const float* noisy, int64_t rows, int64_t cols, const nlem_params* params,
@@ -408,7 +427,8 @@ nlem_status nlm_denoise(const float* noisy, int64_t rows, int64_t cols, const nl
   if (params == nullptr) return invalid(failure, "params must not be null");
   nlem_params p = *params;
   p.solver = NLEM_SOLVER_NLM_ONLY;  // centre of the weighted-mean patch (test_denoise.cpp:228-240)
-  return nlem_denoise_rows(noisy, 0, rows, rows, cols, 0, rows, &p, out, nullptr, failure, stream);
+  return denoise_rows_impl(noisy, 0, rows, rows, cols, 0, rows, &p, out, nullptr, failure, stream,
+                           1);
 }
 
 nlem_status nlem_admm_batched_host(const float* points, const float* weights, int64_t batch,

@@ -9,28 +9,36 @@
 
 namespace nlemk {
 
-// z = weighted mean of the points (types.hpp:71-74 / nlem.cpp:17): sum_k w_k a_k / sum_k w_k,
-// fixed reduction order.  n == 1 gives a_0 exactly (the reference's a * (w/w)).
+// z = weighted mean of the points.  Default: the reference's points * (w / sum w)
+// (types.hpp:71-74, nlem.cpp:17), which stays finite when sum w overflows; with
+// `ratio`: sum_k w_k a_k / sum_k w_k, nlm_denoise's form (nlm.cpp:44).  Fixed
+// reduction order.  n == 1 gives a_0 exactly (a * (w/w)).
 template <int JPL>
-__device__ void block_weighted_mean(const float* a, const float* w, int n, int d, GenWork& W) {
+__device__ void block_weighted_mean(const float* a, const float* w, int n, int d, GenWork& W,
+                                    bool ratio = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (n == 1) {
     for (int j = tid; j < d; j += kGenThreads) W.z[j] = a[j];
     __syncthreads();
     return;
   }
+  float den = 0.0f;
+  for (int k = warp; k < n; k += kGenWarps) den += w[k];
+  if (lane == 0) W.red[warp] = den;
+  __syncthreads();
+  float D = 0.0f;
+#pragma unroll
+  for (int i = 0; i < kGenWarps; ++i) D += W.red[i];
   float num[JPL];
 #pragma unroll
   for (int q = 0; q < JPL; ++q) num[q] = 0.0f;
-  float den = 0.0f;
   for (int k = warp; k < n; k += kGenWarps) {
     const float* ak = a + static_cast<size_t>(k) * d;
-    const float wk = w[k];
-    den += wk;
+    const float c = ratio ? w[k] : w[k] / D;
 #pragma unroll
     for (int q = 0; q < JPL; ++q) {
       const int j = lane + 32 * q;
-      if (j < d) num[q] = fmaf(wk, ak[j], num[q]);
+      if (j < d) num[q] = fmaf(ak[j], c, num[q]);
     }
   }
 #pragma unroll
@@ -38,16 +46,12 @@ __device__ void block_weighted_mean(const float* a, const float* w, int n, int d
     const int j = lane + 32 * q;
     if (j < d) W.gpart[warp * W.dstride + j] = num[q];
   }
-  if (lane == 0) W.red[warp] = den;
   __syncthreads();
-  float D = 0.0f;
-#pragma unroll
-  for (int i = 0; i < kGenWarps; ++i) D += W.red[i];
   for (int j = tid; j < d; j += kGenThreads) {
     float g = 0.0f;
 #pragma unroll
     for (int i = 0; i < kGenWarps; ++i) g += W.gpart[i * W.dstride + j];
-    W.z[j] = g / D;
+    W.z[j] = ratio ? g / D : g;
   }
   __syncthreads();
 }
@@ -74,9 +78,10 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
                      FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   const size_t nd = static_cast<size_t>(n) * d;
+  const size_t ns = admm_state_floats(n, d);
   float* a_s = smem;
   float* p_s = SMEM ? smem + nd : nullptr;
-  GenWork W = carve_gen_work(SMEM ? smem + 2 * nd : smem, n, d);
+  GenWork W = carve_gen_work(SMEM ? smem + nd + ns : smem, n, d);
   const int tid = threadIdx.x;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     const float* ag = points + b * nd;
@@ -88,7 +93,7 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
       p = p_s;
     } else {
       a = ag;
-      p = scratch + blockIdx.x * nd;
+      p = scratch + blockIdx.x * ns;
     }
     for (int k = tid; k < n; k += kGenThreads) W.wts[k] = weights[b * n + k];
     __syncthreads();
@@ -220,9 +225,10 @@ nlem_pixels_generic(const float* __restrict__ pad, int64_t pad_row0, int64_t pad
   const int d = k * k;
   const int nmax = P.search * P.search;
   const size_t ndm = static_cast<size_t>(nmax) * d;
-  float* a_s = SMEM ? smem : scratch + blockIdx.x * 2 * ndm;
+  const size_t nsm = static_cast<size_t>(nmax) * d * (d <= kRefFormMaxDim ? 2 : 1);
+  float* a_s = SMEM ? smem : scratch + blockIdx.x * (ndm + nsm);
   float* p_s = a_s + ndm;
-  GenWork W = carve_gen_work(SMEM ? smem + 2 * ndm : smem, nmax, d);
+  GenWork W = carve_gen_work(SMEM ? smem + ndm + nsm : smem, nmax, d);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int center = d / 2;
   const int64_t plane = out_rows * cols;
@@ -236,7 +242,7 @@ nlem_pixels_generic(const float* __restrict__ pad, int64_t pad_row0, int64_t pad
     // gather patches: a[kk][j] = pad(r0 + kk/nc + dr, c0 + kk%nc + dc)
     for (int e = tid; e < n * d; e += kGenThreads) {
       const int kk = e / d, j = e - kk * d;
-      const int64_t pr = r0 + kk / nc + (j / k - hk) - pad_row0 + hk;
+      const int64_t pr = r0 + kk / nc + (j / k - hk) - pad_row0;
       const int64_t pc = c0 + kk % nc + (j % k - hk) + hk;
       a_s[e] = __ldg(pad + pr * pad_cols + pc);
     }
@@ -254,7 +260,7 @@ nlem_pixels_generic(const float* __restrict__ pad, int64_t pad_row0, int64_t pad
     __syncthreads();
     const bool nlm_init = P.solver == NLEM_SOLVER_NLM_ONLY || P.init_mode == NLEM_INIT_NLM_PATCH;
     if (nlm_init) {
-      block_weighted_mean<JPL>(a_s, W.wts, n, d, W);
+      block_weighted_mean<JPL>(a_s, W.wts, n, d, W, P.nlm_ratio != 0);
     } else {
       for (int j = tid; j < d; j += kGenThreads) W.z[j] = a_s[self * d + j];
       __syncthreads();
@@ -315,8 +321,9 @@ int jpl_for(int d) {
 cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
   const DeviceCaps& caps = device_caps();
   const size_t nd = static_cast<size_t>(L.n) * L.d;
+  const size_t ns = admm_state_floats(L.n, L.d);
   const size_t work = gen_work_floats(L.n, L.d) * sizeof(float);
-  const size_t smem_full = 2 * nd * sizeof(float) + work;
+  const size_t smem_full = (nd + ns) * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
   const size_t smem = use_smem ? smem_full : work;
   const int per_sm = use_smem ? std::max<int>(1, static_cast<int>(caps.smem_per_sm / (smem + 1024))) : 2;
@@ -324,7 +331,7 @@ cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
   grid = std::max<int64_t>(grid, 1);
   float* scratch = nullptr;
   if (!use_smem) {
-    cudaError_t e = cudaMallocAsync(&scratch, grid * nd * sizeof(float), stream);
+    cudaError_t e = cudaMallocAsync(&scratch, grid * ns * sizeof(float), stream);
     if (e != cudaSuccess) return e;
   }
   cudaError_t err = cudaSuccess;
@@ -393,8 +400,9 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream) {
   const int d = L.P.patch * L.P.patch;
   const int nmax = L.P.search * L.P.search;
   const size_t ndm = static_cast<size_t>(nmax) * d;
+  const size_t nsm = static_cast<size_t>(nmax) * d * (d <= kRefFormMaxDim ? 2 : 1);
   const size_t work = gen_work_floats(nmax, d) * sizeof(float);
-  const size_t smem_full = 2 * ndm * sizeof(float) + work;
+  const size_t smem_full = (ndm + nsm) * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
   const size_t smem = use_smem ? smem_full : work;
   const int per_sm = std::max<int>(1, static_cast<int>(caps.smem_per_sm / (smem + 1024)));
@@ -403,7 +411,7 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream) {
   grid = std::max<int64_t>(grid, 1);
   float* scratch = nullptr;
   if (!use_smem) {
-    cudaError_t e = cudaMallocAsync(&scratch, grid * 2 * ndm * sizeof(float), stream);
+    cudaError_t e = cudaMallocAsync(&scratch, grid * (ndm + nsm) * sizeof(float), stream);
     if (e != cudaSuccess) return e;
   }
   NLEM_DISPATCH_JPL(d, {

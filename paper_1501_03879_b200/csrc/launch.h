@@ -61,6 +61,7 @@ struct NlemDevParams {
   int init_mode;
   nlem_box range;
   float irls_tol;
+  int nlm_ratio;  // nlm_denoise's sum w*a / sum w (nlm.cpp:44) instead of points*(w/sum w)
 };
 
 struct NlemLaunch {

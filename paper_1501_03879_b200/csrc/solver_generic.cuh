@@ -91,96 +91,149 @@ __device__ float block_em_cost(const float* a, const float* w, int n, int d, con
   return tot;
 }
 
-// Reference-form sweep for a single point (n == 1), executed by warp 0; exactly
-// admm.hpp:49-78 in float.  z (block smem) holds z0 on entry, the minimizer on exit.
+// Problems at or below this dimension (and every n == 1 problem) run the reference
+// form of the sweep verbatim: there the primal residual can hit exactly zero in
+// finitely many sweeps (1-D medians, single points: proj/tests/unit/test_solvers.cpp
+// :63-151), and only the reference's own arithmetic reproduces the exact stop.
+constexpr int kRefFormMaxDim = 16;
+
+__host__ __device__ inline bool use_ref_form(int n, int d) { return n == 1 || d <= kRefFormMaxDim; }
+
+// floats of solver state per problem (p-form: p; reference form: x and y)
+__host__ __device__ inline size_t admm_state_floats(int n, int d) {
+  return static_cast<size_t>(n) * d * (use_ref_form(n, d) ? 2 : 1);
+}
+
+// Reference-form block sweep (admm.hpp:49-78 in float): state y (multipliers) and x
+// (local copies), warp per point, per-warp then cross-warp reductions.
 template <int JPL, class OnIter>
-__device__ SolveStatus admm_single_point(const float* a, float w, int d, float* z, nlem_box box,
-                                         float mu, int T, float tol, int res_mode,
-                                         float* trace_obj, float* trace_res, OnIter on_iter) {
-  SolveStatus st{0, -1, 0};
-  const int lane = threadIdx.x & 31;
-  if ((threadIdx.x >> 5) == 0) {
-    const float inv_mu = 1.0f / mu;
-    const float lam = inv_mu * w;
-    float y[JPL], zz[JPL], av[JPL];
+__device__ SolveStatus admm_solve_refform(const float* a, const float* w, float* xs, float* ys,
+                                          int n, int d, GenWork& W, nlem_box box, float mu, int T,
+                                          float tol, float* trace_obj, float* trace_res,
+                                          OnIter on_iter) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const float inv_mu = 1.0f / mu;
+  const float nf = static_cast<float>(n);
+  const bool want_obj = trace_obj != nullptr;
+  SolveStatus st{T, -1, 0};
+  for (size_t e = tid; e < static_cast<size_t>(n) * d; e += kGenThreads) ys[e] = 0.0f;  // admm.hpp:41
+  __syncthreads();
+  for (int t = 1; t <= T; ++t) {
+    float zc[JPL], racc[JPL];
 #pragma unroll
     for (int q = 0; q < JPL; ++q) {
       const int j = lane + 32 * q;
-      y[q] = 0.0f;
-      zz[q] = j < d ? z[j] : 0.0f;
-      av[q] = j < d ? a[j] : 0.0f;
+      zc[q] = j < d ? W.z[j] : 0.0f;
+      racc[q] = 0.0f;
     }
-    for (int t = 1; t <= T; ++t) {
-      st.iterations = t;
-      float v[JPL], pull[JPL], x[JPL];
+    for (int k = warp; k < n; k += kGenWarps) {  // admm.hpp:53-57
+      const float* ak = a + static_cast<size_t>(k) * d;
+      float* yk = ys + static_cast<size_t>(k) * d;
+      float* xk = xs + static_cast<size_t>(k) * d;
+      float v[JPL], pull[JPL], yv[JPL], av[JPL];
       float d2 = 0.0f;
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
-        v[q] = zz[q] - inv_mu * y[q];
+        const int j = lane + 32 * q;
+        yv[q] = j < d ? yk[j] : 0.0f;
+        av[q] = j < d ? ak[j] : 0.0f;
+        v[q] = zc[q] - inv_mu * yv[q];
         pull[q] = v[q] - av[q];
-        d2 = fmaf(pull[q], pull[q], d2);
+        if (j < d) d2 = fmaf(pull[q], pull[q], d2);
       }
+      const float lam = inv_mu * w[k];
       const float dist = sqrtf(warp_sum(d2));
       const float f = lam / dist;
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) {
+        const int j = lane + 32 * q;
+        const float x = lam == 0.0f ? v[q] : (dist <= lam ? av[q] : v[q] - f * pull[q]);
+        if (j < d) {
+          xk[j] = x;
+          racc[q] += x + inv_mu * yv[q];
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < JPL; ++q) {
+      const int j = lane + 32 * q;
+      if (j < d) W.gpart[warp * W.dstride + j] = racc[q];
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int j = tid; j < d; j += kGenThreads) {  // admm.hpp:59
+      float r = 0.0f;
+#pragma unroll
+      for (int i = 0; i < kGenWarps; ++i) r += W.gpart[i * W.dstride + j];
+      const float zn = clamp_box(r / nf, box);
+      W.z[j] = zn;
+      bad |= !isfinite(zn);
+    }
+    __syncthreads();
+    float rmax = 0.0f, oacc = 0.0f;
+    bool rfin = true;
+    for (int k = warp; k < n; k += kGenWarps) {  // admm.hpp:61-65
+      const float* ak = a + static_cast<size_t>(k) * d;
+      float* yk = ys + static_cast<size_t>(k) * d;
+      const float* xk = xs + static_cast<size_t>(k) * d;
       float r2 = 0.0f, o2 = 0.0f;
 #pragma unroll
       for (int q = 0; q < JPL; ++q) {
         const int j = lane + 32 * q;
-        x[q] = lam == 0.0f ? v[q] : (dist <= lam ? av[q] : v[q] - f * pull[q]);
-        const float zn = clamp_box(x[q] + inv_mu * y[q], box);  // r / n with n == 1
-        const float e = x[q] - zn;
         if (j < d) {
+          const float e = xk[j] - W.z[j];
           r2 = fmaf(e, e, r2);
-          o2 = fmaf(zn - av[q], zn - av[q], o2);
+          yk[j] += mu * e;
+          if (want_obj) {
+            const float t = W.z[j] - ak[j];
+            o2 = fmaf(t, t, o2);
+          }
         }
-        y[q] += mu * e;
-        zz[q] = zn;
       }
-      const float residual = sqrtf(warp_sum(r2));
-      bool finite = isfinite(residual);
+      const float nr = sqrtf(warp_sum(r2));
+      rfin &= isfinite(nr);
+      rmax = fmaxf(rmax, nr);
+      if (want_obj) oacc = fmaf(w[k], sqrtf(warp_sum(o2)), oacc);
+    }
+    if (lane == 0) {
+      W.red[warp] = rfin ? rmax : __int_as_float(0x7fc00000);
+      W.red[kGenWarps + warp] = oacc;
+    }
+    bad = __syncthreads_or(bad);
+    float residual = 0.0f, obj = 0.0f;
+    bool fin = true;
 #pragma unroll
-      for (int q = 0; q < JPL; ++q) finite &= (lane + 32 * q >= d) || isfinite(zz[q]);
-      finite = __all_sync(0xffffffffu, finite);
-      if (!finite) {
+    for (int i = 0; i < kGenWarps; ++i) {
+      fin &= isfinite(W.red[i]);
+      residual = fmaxf(residual, W.red[i]);
+      obj += W.red[kGenWarps + i];
+    }
+    __syncthreads();
+    if (bad || !fin) {  // admm.hpp:67-68
+      st.fail_iter = t;
+      st.fail_kind = NLEM_FAIL_ADMM_ITERATE;
+      return st;
+    }
+    if (want_obj) {  // admm.hpp:70-74
+      if (!isfinite(obj)) {
         st.fail_iter = t;
-        st.fail_kind = NLEM_FAIL_ADMM_ITERATE;
-        break;
+        st.fail_kind = NLEM_FAIL_ADMM_OBJECTIVE;
+        return st;
       }
-#pragma unroll
-      for (int q = 0; q < JPL; ++q)
-        if (lane + 32 * q < d) z[lane + 32 * q] = zz[q];
-      __syncwarp();
-      if (trace_obj) {
-        const float obj = w * sqrtf(warp_sum(o2));
-        if (!isfinite(obj)) {
-          st.fail_iter = t;
-          st.fail_kind = NLEM_FAIL_ADMM_OBJECTIVE;
-          break;
-        }
-        if (lane == 0) trace_obj[t - 1] = obj;
-      }
-      if (trace_res && lane == 0) trace_res[t - 1] = residual;
-      on_iter(t, z);
-      if (res_mode != RES_NONE && residual <= tol) break;
+      if (tid == 0) trace_obj[t - 1] = obj;
+    }
+    if (trace_res && tid == 0) trace_res[t - 1] = residual;
+    on_iter(t, W.z);
+    if (residual <= tol) {  // admm.hpp:77
+      st.iterations = t;
+      return st;
     }
   }
-  // broadcast the status from warp 0
-  __shared__ int sh[3];
-  if (threadIdx.x == 0) {
-    sh[0] = st.iterations;
-    sh[1] = st.fail_iter;
-    sh[2] = st.fail_kind;
-  }
-  __syncthreads();
-  st.iterations = sh[0];
-  st.fail_iter = sh[1];
-  st.fail_kind = sh[2];
-  __syncthreads();
   return st;
 }
 
 // Block-wide p-form EM-ADMM on one problem.
-//   a [n][d] points, w [n] weights, p [n][d] state scratch (all smem or global)
+//   a [n][d] points, w [n] weights, p state scratch of admm_state_floats(n, d) floats
 //   W.z holds z0 on entry (visible to all threads), the minimizer on exit.
 // on_iter(t, z) is called by every thread after sweep t (snapshots, nlem.cpp:92-128).
 template <int JPL, class OnIter>
@@ -189,9 +242,10 @@ __device__ SolveStatus admm_solve_generic(const float* a, const float* w, float*
                                           int res_mode, float* trace_obj, float* trace_res,
                                           OnIter on_iter) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (n == 1)
-    return admm_single_point<JPL>(a, w[0], d, W.z, box, mu, T, tol, res_mode, trace_obj, trace_res,
-                                  on_iter);
+  if (use_ref_form(n, d))
+    return admm_solve_refform<JPL>(a, w, p + static_cast<size_t>(n) * d, p, n, d, W, box, mu, T,
+                                   res_mode == RES_NONE ? -1.0f : tol, trace_obj, trace_res,
+                                   on_iter);
 
   const float inv_mu = 1.0f / mu;
   const float nf = static_cast<float>(n);
