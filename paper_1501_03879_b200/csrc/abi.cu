@@ -362,12 +362,12 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     return invalid(failure, "input rows outside the image");
   if (out_rows == 0) return NLEM_OK;
   if (!noisy || !out) return invalid(failure, "null buffer");
-  const int hs = params->search / 2, hk = params->patch / 2;
-  const int64_t win_r0 = std::max<int64_t>(0, out_row0 - hs);
-  const int64_t win_r1 = std::min<int64_t>(rows, out_row0 + out_rows + hs);
-  const int64_t pad_row0 = win_r0 - hk;
-  const int64_t pad_rows = (win_r1 - win_r0) + 2 * hk;
-  const int64_t pad_cols = cols + 2 * hk;
+  // Mirror-padded band with a border of S/2 + k/2 on every side, so every patch of the
+  // full (unclipped) S x S window grid around each output pixel is addressable.
+  const int hb = params->search / 2 + params->patch / 2;
+  const int64_t pad_row0 = out_row0 - hb;
+  const int64_t pad_rows = out_rows + 2 * hb;
+  const int64_t pad_cols = cols + 2 * hb;
   for (int64_t r = pad_row0; r < pad_row0 + pad_rows; ++r) {
     const int64_t g = mirror_host(r, rows);
     if (g < in_row0 || g >= in_row0 + in_rows)
@@ -388,7 +388,7 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
   DevSlot slot(s);
   e = slot.init();
   if (e == cudaSuccess)
-    e = launch_pad_band(noisy, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hk, s);
+    e = launch_pad_band(noisy, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hb, s);
   if (e == cudaSuccess) {
     NlemDevParams dp = dev_params(*params);
     dp.nlm_ratio = nlm_ratio;

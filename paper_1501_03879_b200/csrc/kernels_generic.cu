@@ -182,17 +182,17 @@ __device__ __forceinline__ int64_t mirror_index_dev(int64_t i, int64_t n) {
   return m < n ? m : period - m;
 }
 
-// Mirror-padded band: pad[pr][pc] = image(mirror(pad_row0 + pr), mirror(pc - hk)).
+// Mirror-padded band: pad[pr][pc] = image(mirror(pad_row0 + pr), mirror(pc - col_off)).
 // TMA has no mirror mode, so padding once keeps every later patch read in bounds.
 __global__ void pad_band_kernel(const float* __restrict__ in, int64_t in_row0, int64_t rows,
                                 int64_t cols, float* __restrict__ pad, int64_t pad_row0,
-                                int64_t pad_rows, int64_t pad_cols, int hk) {
+                                int64_t pad_rows, int64_t pad_cols, int col_off) {
   const int64_t total = pad_rows * pad_cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t pr = i / pad_cols, pc = i - pr * pad_cols;
     const int64_t gr = mirror_index_dev(pad_row0 + pr, rows);
-    const int64_t gc = mirror_index_dev(pc - hk, cols);
+    const int64_t gc = mirror_index_dev(pc - col_off, cols);
     pad[i] = in[(gr - in_row0) * cols + gc];
   }
 }
@@ -243,7 +243,7 @@ nlem_pixels_generic(const float* __restrict__ pad, int64_t pad_row0, int64_t pad
     for (int e = tid; e < n * d; e += kGenThreads) {
       const int kk = e / d, j = e - kk * d;
       const int64_t pr = r0 + kk / nc + (j / k - hk) - pad_row0;
-      const int64_t pc = c0 + kk % nc + (j % k - hk) + hk;
+      const int64_t pc = c0 + kk % nc + (j % k - hk) + hs + hk;  // pad col 0 = global -(hs+hk)
       a_s[e] = __ldg(pad + pr * pad_cols + pc);
     }
     __syncthreads();
