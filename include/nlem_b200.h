@@ -144,6 +144,12 @@ nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t
                               float* objective_out, int32_t* iters_out, float* trace_objective,
                               nlem_failure* failure, void* stream);
 
+/* Same contract on host buffers. */
+nlem_status nlem_irls_batched_host(const float* points, const float* weights, int64_t batch,
+                                   int64_t n, int64_t d, const float* x_init, nlem_irls_config cfg,
+                                   float* x_out, float* objective_out, int32_t* iters_out,
+                                   float* trace_objective, nlem_failure* failure, int32_t device);
+
 /*
  * Whole-image NLEM (proj/src/nlem.cpp:68-90).  noisy/out [rows][cols] device.
  * frames: NULL, or [solver_iters][rows][cols] device receiving

@@ -49,7 +49,8 @@ class ParamsC(C.Structure):
 # Every symbol include/nlem_b200.h declares (checked by tests/test_abi_cpu.py).
 EXPORTS = [
     "nlem_version", "nlem_status_string", "nlem_validate_params", "nlem_default_init_mode",
-    "nlem_admm_batched", "nlem_admm_batched_host", "nlem_irls_batched", "nlem_denoise",
+    "nlem_admm_batched", "nlem_admm_batched_host", "nlem_irls_batched",
+    "nlem_irls_batched_host", "nlem_denoise",
     "nlem_denoise_rows", "nlem_denoise_rows_host", "nlem_denoise_host", "nlm_denoise", "nlem_band_halo",
     "nlem_add_gaussian_noise", "nlem_synth_clean_image", "nlem_synth_noisy_image",
     "nlem_synth_point_sets",
@@ -84,6 +85,8 @@ def load(build_if_missing: bool = True):
                                          C.c_int32]
     L.nlem_irls_batched.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, IrlsConfigC, vp,
                                     vp, vp, vp, C.POINTER(Failure), vp]
+    L.nlem_irls_batched_host.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int64, vp, IrlsConfigC,
+                                         vp, vp, vp, vp, C.POINTER(Failure), C.c_int32]
     L.nlem_denoise.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(ParamsC), vp, vp,
                                C.POINTER(Failure), vp]
     L.nlem_denoise_rows.argtypes = [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int64,

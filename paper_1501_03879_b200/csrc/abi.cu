@@ -486,6 +486,56 @@ nlem_status nlem_admm_batched_host(const float* points, const float* weights, in
   return st;
 }
 
+nlem_status nlem_irls_batched_host(const float* points, const float* weights, int64_t batch,
+                                   int64_t n, int64_t d, const float* x_init, nlem_irls_config cfg,
+                                   float* x_out, float* objective_out, int32_t* iters_out,
+                                   float* trace_objective, nlem_failure* failure, int32_t device) {
+  nlem_failure local;
+  nlem_failure* f = failure ? failure : &local;
+  clear(f);
+  if (batch <= 0 || n < 1 || d < 1)
+    return nlem_irls_batched(nullptr, nullptr, batch, n, d, nullptr, cfg, nullptr, nullptr, nullptr,
+                             nullptr, f, nullptr);
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  cudaStream_t s = cudaStreamPerThread;
+  const size_t P = static_cast<size_t>(batch) * n * d, Wn = static_cast<size_t>(batch) * n,
+               Z = static_cast<size_t>(batch) * d,
+               Tn = static_cast<size_t>(batch) * std::max(cfg.max_iter, 1);
+  float *dp = nullptr, *dw = nullptr, *dxi = nullptr, *dx = nullptr, *dob = nullptr, *dto = nullptr;
+  int32_t* dit = nullptr;
+  auto alloc = [&](void** p, size_t bytes) {
+    if (e == cudaSuccess) e = cudaMallocAsync(p, bytes, s);
+  };
+  alloc(reinterpret_cast<void**>(&dp), P * 4);
+  alloc(reinterpret_cast<void**>(&dw), Wn * 4);
+  alloc(reinterpret_cast<void**>(&dx), Z * 4);
+  if (x_init) alloc(reinterpret_cast<void**>(&dxi), Z * 4);
+  if (objective_out) alloc(reinterpret_cast<void**>(&dob), batch * 4);
+  if (iters_out) alloc(reinterpret_cast<void**>(&dit), batch * 4);
+  if (trace_objective) alloc(reinterpret_cast<void**>(&dto), Tn * 4);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, points, P * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, weights, Wn * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && dxi) e = cudaMemcpyAsync(dxi, x_init, Z * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess && dto) e = cudaMemcpyAsync(dto, trace_objective, Tn * 4, cudaMemcpyHostToDevice, s);
+  nlem_status st = NLEM_OK;
+  if (e == cudaSuccess) st = nlem_irls_batched(dp, dw, batch, n, d, dxi, cfg, dx, dob, dit, dto, f, s);
+  if (e == cudaSuccess && st == NLEM_OK) {
+    e = cudaMemcpyAsync(x_out, dx, Z * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dob) e = cudaMemcpyAsync(objective_out, dob, batch * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dit) e = cudaMemcpyAsync(iters_out, dit, batch * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && dto) e = cudaMemcpyAsync(trace_objective, dto, Tn * 4, cudaMemcpyDeviceToHost, s);
+  }
+  for (void* p : {static_cast<void*>(dp), static_cast<void*>(dw), static_cast<void*>(dxi),
+                  static_cast<void*>(dx), static_cast<void*>(dob), static_cast<void*>(dit),
+                  static_cast<void*>(dto)})
+    if (p) cudaFreeAsync(p, s);
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  return st;
+}
+
 nlem_status nlem_denoise_rows_host(const float* noisy, int64_t in_row0, int64_t in_rows,
                                    int64_t rows, int64_t cols, int64_t out_row0, int64_t out_rows,
                                    const nlem_params* params, float* out, float* frames,
