@@ -16,7 +16,7 @@ OUT_DIR = os.path.join(HERE, "_lib")
 SO = os.path.join(OUT_DIR, "libnlem_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu"]
+CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu"]
 CXX_SOURCES = ["synth.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

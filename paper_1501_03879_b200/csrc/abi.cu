@@ -394,7 +394,9 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
-    e = nlem_fast_supported(L) ? launch_nlem_fast(L, s) : launch_nlem_generic(L, s);
+    e = nlem_tile_supported(L)   ? launch_nlem_tile(L, s)
+        : nlem_fast_supported(L) ? launch_nlem_fast(L, s)
+                                 : launch_nlem_generic(L, s);
   }
   cudaFreeAsync(pad, s);
   if (e != cudaSuccess) return cuda_fail(failure, e);

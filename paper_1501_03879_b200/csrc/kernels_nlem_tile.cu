@@ -1,0 +1,504 @@
+// Tile-reuse NLEM kernel (configs 0, 2, 3): the patch stack is never materialised.
+//
+// A pixel's S x S window grid of patches (k x k each) is a sliding-window view of one
+// (S+k-1)^2 image tile.  Lane (group q, patch row dr) owns KB consecutive grid points
+// (gr, gc0..gc0+KB-1) x the k coordinates of patch row dr, so the KB*k elements it touches
+// are a_{m,dc} = tile[gr+dr][gc0+m+dc]: only KB+k-1 distinct values.  They are loaded ONCE
+// per pixel into registers (as even- and odd-aligned float2 pairs, from two shifted smem
+// copies of the tile), next to the p-form state p_{m,dc} (solver_generic.cuh), so a sweep
+// reads no point data from shared memory at all.  Per sweep and lane: FADD2/FFMA2 update
+// and norm partials over point pairs, a shared-memory transpose of the per-point norm
+// partials across the k lanes of the group, one prox scale per lane (rsqrt), a shuffle
+// broadcast, g partials, then one CTA barrier and a multi-thread consensus per coordinate.
+#include <algorithm>
+
+#include "launch.h"
+#include "solver_generic.cuh"
+
+namespace nlemk {
+
+template <int KS_, int SW_, int KB_>
+struct TileCfg {
+  static constexpr int KS = KS_;                 // patch side k
+  static constexpr int SW = SW_;                 // search window side S
+  static constexpr int KB = KB_;                 // grid points per lane (one grid-row segment)
+  static constexpr int D = KS * KS;
+  static constexpr int G = KS;                   // lanes per group = patch rows
+  static constexpr int GPW = 32 / G;             // groups per warp
+  static constexpr int NBLK = SW / KB;           // segments per grid row
+  static constexpr int NGROUPS = SW * NBLK;
+  static constexpr int WARPS = (NGROUPS + GPW - 1) / GPW;
+  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int KP = KB / 2;              // point pairs per lane
+  static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
+  static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
+  static constexpr int TH = SW + KS - 1;         // tile side
+  static constexpr int TWS = (TH + 4) & ~1;      // tile row stride (even, with slack)
+  static constexpr int NE = ((KP - 1 + (KS - 1) / 2) > ((SEG - 1) / 2) ? (KP - 1 + (KS - 1) / 2)
+                                                                        : ((SEG - 1) / 2)) + 1;
+  static constexpr int NO = KP - 1 + (KS - 2) / 2 + 1;
+  static constexpr int KBP = (KB + 3) & ~3;      // padded per-lane norm row
+  static constexpr int KSP = (KS + 3) & ~3;      // padded per-lane coordinate row
+  static constexpr int SPL = (KB + G - 1) / G;   // points whose prox scale a lane computes
+  static constexpr int CPT = THREADS >= 8 * D ? 8 : THREADS >= 4 * D ? 4 : THREADS >= 2 * D ? 2 : 1;
+  static_assert(SW % KB == 0, "segments tile the grid row");
+  static_assert(D <= THREADS, "consensus needs one thread per coordinate");
+};
+
+using TileK7S21 = TileCfg<7, 21, 7>;   // configs 2, 3: 63 groups of 7 lanes, 16 warps
+using TileK5S11 = TileCfg<5, 11, 11>;  // config 0: 11 groups of 5 lanes, 2 warps
+
+template <class C>
+struct TileSmem {
+  static constexpr int T = C::TH * C::TWS;            // one tile copy
+  static constexpr int NB = C::NGROUPS * C::G * C::KBP;  // norm transpose
+  static constexpr int RED = C::NGROUPS * C::G * C::KSP; // g / init partials
+  static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
+                               C::NGROUPS * C::KBP /*w*/ + 64;
+};
+
+__device__ __forceinline__ float2 tf2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 tsub2(float2 a, float2 b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+__device__ __forceinline__ float2 tfma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+
+// Per-lane register image of its tile segment t[0..SEG): E[i] = (t[2i], t[2i+1]),
+// O[i] = (t[2i+1], t[2i+2]).  a_{m,dc} = t[m+dc].
+template <class C>
+struct Seg {
+  float2 E[C::NE];
+  float2 O[C::NO];
+  // float2 of the point pair (2q, 2q+1) at coordinate dc
+  __device__ __forceinline__ float2 pair(int q, int dc) const {
+    return (dc & 1) ? O[q + (dc - 1) / 2] : E[q + dc / 2];
+  }
+  // the unpaired point m = KB-1 at coordinate dc
+  __device__ __forceinline__ float single(int dc) const {
+    const int x = C::KB - 1 + dc;
+    return (x & 1) ? E[x / 2].y : E[x / 2].x;
+  }
+};
+
+template <class C>
+struct TileCtx {
+  float* T0;    // tile
+  float* T1;    // tile shifted left by one column
+  float* nbuf;  // [NGROUPS][G][KBP]
+  float* red;   // [NGROUPS][G][KSP]
+  float2* c2;   // [D]
+  float* z;     // [D]
+  float* a0;    // [D]
+  float* wbuf;  // [NGROUPS][KBP]
+  int* flags;   // [4]
+  float* scal;  // [32]
+  int tid, warp, lane, q, dr, base;
+  bool active;  // lane belongs to a real group
+  int gr, gc0;  // grid row and first grid column of the lane's segment
+
+  __device__ void carve(float* smem) {
+    T0 = smem;
+    T1 = T0 + TileSmem<C>::T;
+    nbuf = T1 + TileSmem<C>::T;
+    red = nbuf + TileSmem<C>::NB;
+    c2 = reinterpret_cast<float2*>(red + TileSmem<C>::RED);
+    z = reinterpret_cast<float*>(c2 + C::D);
+    a0 = z + C::D;
+    wbuf = a0 + C::D;
+    flags = reinterpret_cast<int*>(wbuf + C::NGROUPS * C::KBP);
+    scal = reinterpret_cast<float*>(flags + 8);
+    tid = threadIdx.x;
+    warp = tid >> 5;
+    lane = tid & 31;
+    const int ql = lane / C::G;
+    dr = lane - ql * C::G;
+    base = ql * C::G;
+    q = warp * C::GPW + ql;
+    active = ql < C::GPW && q < C::NGROUPS;
+    const int qq = active ? q : 0;
+    gr = qq / C::NBLK;
+    gc0 = (qq % C::NBLK) * C::KB;
+  }
+};
+
+// Transpose-reduce per-point partials across the G lanes of a group through shared memory:
+// v[m] = this lane's partial for point m (m < KB); returns, for the SPL points m = dr + i*G
+// this lane owns, the group totals.  Fixed summation order (lanes 0..G-1).
+template <class C>
+__device__ __forceinline__ void group_point_totals(TileCtx<C>& X, const float (&v)[C::KB],
+                                                   float (&tot)[C::SPL]) {
+  float* row = X.nbuf + (X.q * C::G + X.dr) * C::KBP;
+  if (X.active)
+#pragma unroll
+    for (int m = 0; m < C::KB; ++m) row[m] = v[m];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < C::SPL; ++i) {
+    const int m = X.dr + i * C::G;
+    float t = 0.0f;
+    if (X.active && m < C::KB) {
+      const float* col = X.nbuf + X.q * C::G * C::KBP + m;
+#pragma unroll
+      for (int r = 0; r < C::G; ++r) t += col[r * C::KBP];
+    }
+    tot[i] = t;
+  }
+  __syncwarp();
+}
+
+// Broadcast per-point values (owned by lane m % G, slot m / G) to every lane of the group.
+template <class C>
+__device__ __forceinline__ void group_broadcast(const TileCtx<C>& X, const float (&own)[C::SPL],
+                                                float (&all)[C::KB]) {
+#pragma unroll
+  for (int m = 0; m < C::KB; ++m) {
+    float v = own[0];
+#pragma unroll
+    for (int i = 1; i < C::SPL; ++i)
+      if (m / C::G == i) v = own[i];
+    all[m] = __shfl_sync(0xffffffffu, v, X.base + m % C::G);
+  }
+}
+
+// Sum the per-lane coordinate partials v[dc] (coordinate j = dr*KS + dc) over all groups:
+// lanes write red[q][dr][dc]; after a barrier CPT threads per coordinate sum groups in a
+// fixed order and `finish(j, total)` runs on one thread per coordinate.  Ends with a barrier.
+template <class C, class Finish>
+__device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&v)[C::KS],
+                                                   Finish finish) {
+  if (X.active) {
+    float* row = X.red + (X.q * C::G + X.dr) * C::KSP;
+#pragma unroll
+    for (int dc = 0; dc < C::KS; ++dc) row[dc] = v[dc];
+  }
+  __syncthreads();
+  const int j = X.tid / C::CPT, part = X.tid % C::CPT;
+  float s = 0.0f;
+  if (j < C::D) {
+    const int jr = j / C::KS, jc = j - jr * C::KS;
+    const float* col = X.red + jr * C::KSP + jc;
+    for (int g = part; g < C::NGROUPS; g += C::CPT) s += col[g * C::G * C::KSP];
+  }
+#pragma unroll
+  for (int o = 1; o < C::CPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (j < C::D && part == 0) finish(j, s);
+  __syncthreads();
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, 1)
+nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
+                 int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
+                 int* work_counter, int chunk, FailureSlot* fail) {
+  extern __shared__ __align__(16) float smem[];
+  TileCtx<C> X;
+  X.carve(smem);
+  __shared__ int next_chunk;
+  constexpr int hs = C::SW / 2;
+  constexpr int center = C::D / 2;
+  const int64_t plane = out_rows * cols;
+  const int64_t nchunks = (plane + chunk - 1) / chunk;
+  const float inv_mu = 1.0f / P.mu;
+  // lane-constant tile addressing of the segment (row gr+dr, columns gc0..gc0+SEG)
+  const int trow = X.gr + X.dr;
+  const bool even = (X.gc0 & 1) == 0;
+  const int offE = trow * C::TWS + (even ? X.gc0 : X.gc0 - 1);
+  const int offO = trow * C::TWS + (even ? X.gc0 : X.gc0 + 1);
+  const bool useT1E = !even, useT1O = even;
+  // zero the tile slack columns once
+  for (int e = X.tid; e < 2 * TileSmem<C>::T; e += C::THREADS) X.T0[e] = 0.0f;
+  __syncthreads();
+
+  for (;;) {
+    if (X.tid == 0) next_chunk = atomicAdd(work_counter, 1);
+    __syncthreads();
+    const int64_t ch = next_chunk;
+    __syncthreads();
+    if (ch >= nchunks) break;
+    const int64_t pix_end = (ch + 1) * chunk < plane ? (ch + 1) * chunk : plane;
+    for (int64_t pix = ch * chunk; pix < pix_end; ++pix) {
+      const int64_t r = out_row0 + pix / cols, c = pix % cols;
+      const int gr0 = r < hs ? static_cast<int>(hs - r) : 0;
+      const int gr1 = rows - 1 - r < hs ? static_cast<int>(hs + (rows - 1 - r)) : C::SW - 1;
+      const int gc0w = c < hs ? static_cast<int>(hs - c) : 0;
+      const int gc1w = cols - 1 - c < hs ? static_cast<int>(hs + (cols - 1 - c)) : C::SW - 1;
+      const int n = (gr1 - gr0 + 1) * (gc1w - gc0w + 1);
+      const float inv_n = 1.0f / static_cast<float>(n);
+      // ---- tile (and its one-column-shifted copy) from the padded band
+      const float* src = pad + (r - out_row0) * pad_cols + c;
+      for (int e = X.tid; e < C::TH * C::TH; e += C::THREADS) {
+        const int tr = e / C::TH, tc = e - tr * C::TH;
+        const float v = __ldg(src + tr * pad_cols + tc);
+        X.T0[tr * C::TWS + tc] = v;
+        if (tc > 0) X.T1[tr * C::TWS + tc - 1] = v;
+      }
+      __syncthreads();
+      // footprint-constancy (all real patches equal <=> exact-stop candidate) and a0
+      const float ref = X.T0[gr0 * C::TWS + gc0w];
+      int neq = 0;
+      for (int e = X.tid; e < C::TH * C::TH; e += C::THREADS) {
+        const int tr = e / C::TH, tc = e - tr * C::TH;
+        if (tr >= gr0 && tr <= gr1 + C::KS - 1 && tc >= gc0w && tc <= gc1w + C::KS - 1)
+          neq |= X.T0[tr * C::TWS + tc] != ref;
+      }
+      if (X.tid < C::D) X.a0[X.tid] = ref;
+      if (X.tid == 0) {
+        X.flags[0] = 0;
+        X.flags[1] = 0;
+      }
+      // ---- segment registers
+      Seg<C> S;
+      {
+        const float2* pE = reinterpret_cast<const float2*>((useT1E ? X.T1 : X.T0) + offE);
+        const float2* pO = reinterpret_cast<const float2*>((useT1O ? X.T1 : X.T0) + offO);
+#pragma unroll
+        for (int i = 0; i < C::NE; ++i) S.E[i] = pE[i];
+#pragma unroll
+        for (int i = 0; i < C::NO; ++i) S.O[i] = pO[i];
+      }
+      const bool static_eq = !__syncthreads_or(neq);
+      // is grid point m of my segment a real neighbour (inside the clipped window)?
+      const bool row_real = X.active && X.gr >= gr0 && X.gr <= gr1;
+      auto is_real = [&](int m) {
+        const int gc = X.gc0 + m;
+        return row_real && m < C::KB && gc >= gc0w && gc <= gc1w;
+      };
+      // ---- similarity weights w_m = exp(-||P_m - P_self||^2 / h^2)  (patch.cpp:52-61)
+      float wown[C::SPL];
+      {
+        float sv[C::KS];
+#pragma unroll
+        for (int dc = 0; dc < C::KS; ++dc) sv[dc] = X.T0[(hs + X.dr) * C::TWS + hs + dc];
+        float d2[C::KB];
+#pragma unroll
+        for (int qq = 0; qq < C::KP; ++qq) {
+          float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int dc = 0; dc < C::KS; ++dc) {
+            const float2 e = tsub2(S.pair(qq, dc), tf2(sv[dc]));
+            acc = tfma2(e, e, acc);
+          }
+          d2[2 * qq] = acc.x;
+          d2[2 * qq + 1] = acc.y;
+        }
+        if (C::ODD) {
+          float acc = 0.0f;
+#pragma unroll
+          for (int dc = 0; dc < C::KS; ++dc) {
+            const float e = S.single(dc) - sv[dc];
+            acc = fmaf(e, e, acc);
+          }
+          d2[C::KB - 1] = acc;
+        }
+        float tot[C::SPL];
+        group_point_totals<C>(X, d2, tot);
+#pragma unroll
+        for (int i = 0; i < C::SPL; ++i) {
+          const int m = X.dr + i * C::G;
+          wown[i] = is_real(m) ? expf(-tot[i] * P.inv_h2) : 0.0f;
+        }
+      }
+      float wall[C::KB];
+      group_broadcast<C>(X, wown, wall);
+      // ---- initial patch (nlem.cpp:13-18)
+      const bool nlm_init = P.solver == NLEM_SOLVER_NLM_ONLY || P.init_mode == NLEM_INIT_NLM_PATCH;
+      if (nlm_init) {
+        // W = sum of weights (each point counted once by its owner lane)
+        float wsum = 0.0f;
+#pragma unroll
+        for (int i = 0; i < C::SPL; ++i) wsum += wown[i];
+        wsum = warp_sum(X.active ? wsum : 0.0f);
+        if (X.lane == 0) X.scal[X.warp] = wsum;
+        __syncthreads();
+        float W = 0.0f;
+#pragma unroll
+        for (int w = 0; w < C::WARPS; ++w) W += X.scal[w];
+        const bool ratio = P.nlm_ratio != 0;
+        float coef[C::KB];
+#pragma unroll
+        for (int m = 0; m < C::KB; ++m) coef[m] = ratio ? wall[m] : wall[m] / W;
+        float v[C::KS];
+#pragma unroll
+        for (int dc = 0; dc < C::KS; ++dc) {
+          float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int qq = 0; qq < C::KP; ++qq)
+            acc = tfma2(make_float2(coef[2 * qq], coef[2 * qq + 1]), S.pair(qq, dc), acc);
+          float t = acc.x + acc.y;
+          if (C::ODD) t = fmaf(coef[C::KB - 1], S.single(dc), t);
+          v[dc] = X.active ? t : 0.0f;
+        }
+        reduce_coordinates<C>(X, v, [&](int j, float tsum) { X.z[j] = ratio ? tsum / W : tsum; });
+      } else {
+        if (X.tid < C::D) {
+          const int jr = X.tid / C::KS, jc = X.tid - jr * C::KS;
+          X.z[X.tid] = X.T0[(hs + jr) * C::TWS + hs + jc];
+        }
+        __syncthreads();
+      }
+
+      int iters = P.iters, fail_iter = -1, fail_kind = 0;
+      if (P.solver == NLEM_SOLVER_ADMM) {
+        // ---- EM-ADMM sweeps in p-form (see solver_generic.cuh)
+        float lam_own[C::SPL];
+#pragma unroll
+        for (int i = 0; i < C::SPL; ++i) lam_own[i] = inv_mu * wown[i];
+        float2 p2[C::KP][C::KS];
+        float p1[C::KS];
+        float2 s2[C::KP];
+        float s1 = 0.0f;
+#pragma unroll
+        for (int qq = 0; qq < C::KP; ++qq) {
+          s2[qq] = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int dc = 0; dc < C::KS; ++dc) p2[qq][dc] = make_float2(0.0f, 0.0f);
+        }
+#pragma unroll
+        for (int dc = 0; dc < C::KS; ++dc) p1[dc] = 0.0f;
+        // c of the first sweep = z0 (p = 0*p + z0 - a)
+        if (X.tid < C::D) X.c2[X.tid] = tf2(X.z[X.tid]);
+        __syncthreads();
+        for (int t = 1; t <= P.iters; ++t) {
+          // (U) p' = s p + (c - a); per-point norm partials
+          float nr[C::KB];
+          {
+            float2 cc[C::KS];
+#pragma unroll
+            for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
+#pragma unroll
+            for (int qq = 0; qq < C::KP; ++qq) {
+              float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) {
+                const float2 ca = tsub2(cc[dc], S.pair(qq, dc));
+                p2[qq][dc] = tfma2(s2[qq], p2[qq][dc], ca);
+                acc = tfma2(p2[qq][dc], p2[qq][dc], acc);
+              }
+              nr[2 * qq] = acc.x;
+              nr[2 * qq + 1] = acc.y;
+            }
+            if (C::ODD) {
+              float acc = 0.0f;
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) {
+                p1[dc] = fmaf(s1, p1[dc], cc[dc].x - S.single(dc));
+                acc = fmaf(p1[dc], p1[dc], acc);
+              }
+              nr[C::KB - 1] = acc;
+            }
+          }
+          // (R) group totals -> prox scales -> broadcast
+          float tot[C::SPL], sown[C::SPL];
+          group_point_totals<C>(X, nr, tot);
+          bool ok = true, one = true;
+#pragma unroll
+          for (int i = 0; i < C::SPL; ++i) {
+            const int m = X.dr + i * C::G;
+            const bool rm = is_real(m);
+            float s = 0.0f;
+            if (lam_own[i] != 0.0f) s = fminf(1.0f, lam_own[i] * rsqrtf(tot[i]));
+            sown[i] = s;
+            ok &= isfinite(tot[i]) || !rm;
+            one &= !rm || s == 1.0f;
+          }
+          float sall[C::KB];
+          group_broadcast<C>(X, sown, sall);
+#pragma unroll
+          for (int qq = 0; qq < C::KP; ++qq) s2[qq] = make_float2(sall[2 * qq], sall[2 * qq + 1]);
+          if (C::ODD) s1 = sall[C::KB - 1];
+          // (G) g partials per coordinate
+          float v[C::KS];
+#pragma unroll
+          for (int dc = 0; dc < C::KS; ++dc) {
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int qq = 0; qq < C::KP; ++qq) acc = tfma2(s2[qq], p2[qq][dc], acc);
+            float tsum = acc.x + acc.y;
+            if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
+            v[dc] = X.active ? tsum : 0.0f;
+          }
+          const int wbad = __any_sync(0xffffffffu, !ok);
+          const int wnot1 = __any_sync(0xffffffffu, !one);
+          if (X.lane == 0 && (wbad | wnot1)) atomicOr(&X.flags[t & 1], (wbad ? 1 : 0) | (wnot1 ? 2 : 0));
+          // consensus z_t = P_C(z - g/n), c = 2 z_t - z  (admm.hpp:59-65 in p-form)
+          reduce_coordinates<C>(X, v, [&](int j, float gsum) {
+            const float zo = X.z[j];
+            const float zn = clamp_box(fmaf(-gsum, inv_n, zo), P.range);
+            int f = isfinite(zn) ? 0 : 4;
+            f |= (zn != X.a0[j]) ? 8 : 0;
+            X.z[j] = zn;
+            X.c2[j] = tf2(2.0f * zn - zo);
+            if (f) atomicOr(&X.flags[t & 1], f);
+            if (j == 0) X.flags[(t + 1) & 1] = 0;  // all reads of sweep t-1's word are done
+          });
+          const int fl = X.flags[t & 1];
+          if (fl & (4 | 1)) {
+            fail_iter = (fl & 4) || t == 1 ? t : t - 1;
+            fail_kind = NLEM_FAIL_ADMM_ITERATE;
+            break;
+          }
+          if (frames && X.tid == 0) frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
+          if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
+            iters = t;
+            break;
+          }
+        }
+      }
+      if (X.tid == 0) {
+        if (fail_iter >= 0) {
+          record_failure(fail, r * cols + c, fail_iter, fail_kind);
+        } else {
+          float v = X.z[center];
+          if (P.solver != NLEM_SOLVER_ADMM) v = clamp_box(v, P.range);  // NlmOnly (nlem.cpp:26-31)
+          out[pix] = v;
+          if (frames) {
+            const int from = P.solver == NLEM_SOLVER_ADMM ? iters : 0;
+            for (int t = from; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = v;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+namespace {
+
+template <class C>
+cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
+  const size_t smem = TileSmem<C>::TOTAL * sizeof(float);
+  auto kfn = nlem_pixels_tile<C>;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
+  const int64_t pixels = L.out_rows * L.cols;
+  const int64_t ctas = int64_t(device_caps().sms) * std::max(per_sm, 1);
+  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (ctas * 4))));
+  int* counter = nullptr;
+  e = cudaMallocAsync(&counter, sizeof(int), stream);
+  if (e != cudaSuccess) return e;
+  cudaMemsetAsync(counter, 0, sizeof(int), stream);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, (pixels + chunk - 1) / chunk));
+  kfn<<<static_cast<unsigned>(grid), C::THREADS, smem, stream>>>(
+      L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out, L.frames, counter,
+      chunk, L.fail);
+  e = cudaGetLastError();
+  cudaFreeAsync(counter, stream);
+  return e;
+}
+
+}  // namespace
+
+bool nlem_tile_supported(const NlemLaunch& L) {
+  if (L.P.solver == NLEM_SOLVER_IRLS) return false;
+  return (L.P.patch == 7 && L.P.search == 21) || (L.P.patch == 5 && L.P.search == 11);
+}
+
+cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream) {
+  if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream);
+  return launch_tile<TileK5S11>(L, stream);
+}
+
+}  // namespace nlemk
