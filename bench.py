@@ -151,6 +151,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-rows", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the config-1 / config-2 secondary measurements (N=1 only)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -312,6 +314,15 @@ def main():
                "sample": f"{len(sample)} random full rows ({px} px) of the config-3 image, FP64 "
                          f"oracle restatement, {dt:.1f} s"}
 
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_secondary
+
+        secondary = bench_secondary.measure()
+        secondary["note"] = ("device-resident, CUDA events, L2 flushed; config 1 = BASELINE "
+                             "configs[1] (65,536 x n=441 x d=49, T=50, mu=1), config 2 = 512^2")
+
     value = rows * cols / (total_ms / args.steps / 1e3) / 1e6
     e2e_val = rows * cols / (e2e_s / args.steps) / 1e6
     clk = clocks.summary()
@@ -340,6 +351,7 @@ def main():
         "clocks": clk,
         "gpu_launches": 2 * args.steps,
         "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:

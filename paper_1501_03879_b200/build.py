@@ -16,7 +16,8 @@ OUT_DIR = os.path.join(HERE, "_lib")
 SO = os.path.join(OUT_DIR, "libnlem_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu"]
+CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu",
+              "kernels_nlem_seg2.cu"]
 CXX_SOURCES = ["synth.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -38,30 +39,34 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
+    """variant="prof": debug build with NLEM_PHASE_PROFILE into _lib/libnlem_b200_prof.so."""
+    so = SO if not variant else SO.replace(".so", f"_{variant}.so")
+    if not force and not variant and not _stale():
         return SO
     os.makedirs(OUT_DIR, exist_ok=True)
     objs = []
     for src in sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
-            cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
+            extra = ["-DNLEM_PHASE_PROFILE"] if variant == "prof" else []
+            cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++20", "-fPIC", "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
         objs.append(obj)
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-lpthread"]
     subprocess.run(cmd, check=True)
-    os.replace(tmp, SO)
+    os.replace(tmp, so)
     for o in objs:
         os.remove(o)
-    return SO
+    return so
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True,
+                variant="prof" if "--prof" in sys.argv else ""))

@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -394,9 +395,14 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
-    e = nlem_tile_supported(L)   ? launch_nlem_tile(L, s)
-        : nlem_fast_supported(L) ? launch_nlem_fast(L, s)
-                                 : launch_nlem_generic(L, s);
+    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=seg2|tile|fast|generic
+    // forces one (A/B measurements; falls back to generic when unsupported)
+    static const char* force = std::getenv("NLEM_KERNEL");
+    const std::string k = force ? force : "";
+    if ((k.empty() || k == "tile") && nlem_tile_supported(L)) e = launch_nlem_tile(L, s);
+    else if ((k.empty() || k == "seg2") && nlem_seg2_supported(L)) e = launch_nlem_seg2(L, s);
+    else if ((k.empty() || k == "fast") && nlem_fast_supported(L)) e = launch_nlem_fast(L, s);
+    else e = launch_nlem_generic(L, s);
   }
   cudaFreeAsync(pad, s);
   if (e != cudaSuccess) return cuda_fail(failure, e);

@@ -12,12 +12,29 @@
 // broadcast, g partials, then one CTA barrier and a multi-thread consensus per coordinate.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "launch.h"
 #include "solver_generic.cuh"
 
 namespace nlemk {
 
-template <int KS_, int SW_, int KB_>
+#ifdef NLEM_PHASE_PROFILE
+// Debug-only: clock64 stamps of sweep phases for the first pixels of CTA 0 (warp 0, lane 0
+// and the last warp's lane 0), read back by nlem_debug_phase_times.
+__device__ long long g_phase[2][64][16];
+#define PHASE(slot)                                                                            \
+  do {                                                                                        \
+    if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32) && X.dbg_it < 64) \
+      g_phase[threadIdx.x == 0 ? 0 : 1][X.dbg_it][slot] = clock64();                             \
+  } while (0)
+#else
+#define PHASE(slot) \
+  do {              \
+  } while (0)
+#endif
+
+template <int KS_, int SW_, int KB_, int CL_>
 struct TileCfg {
   static constexpr int KS = KS_;                 // patch side k
   static constexpr int SW = SW_;                 // search window side S
@@ -27,7 +44,9 @@ struct TileCfg {
   static constexpr int GPW = 32 / G;             // groups per warp
   static constexpr int NBLK = SW / KB;           // segments per grid row
   static constexpr int NGROUPS = SW * NBLK;
-  static constexpr int WARPS = (NGROUPS + GPW - 1) / GPW;
+  static constexpr int CL = CL_;                 // CTAs per pixel (thread-block cluster)
+  static constexpr int NGC = (NGROUPS + CL - 1) / CL;  // groups per CTA
+  static constexpr int WARPS = (NGC + GPW - 1) / GPW;
   static constexpr int THREADS = 32 * WARPS;
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
@@ -38,26 +57,38 @@ struct TileCfg {
                                                                         : ((SEG - 1) / 2)) + 1;
   static constexpr int NO = KP - 1 + (KS - 2) / 2 + 1;
   static constexpr int KBP = (KB + 3) & ~3;      // padded per-lane norm row
-  static constexpr int KSP = (KS + 3) & ~3;      // padded per-lane coordinate row
+  static constexpr int KSP = KS;                 // per-lane coordinate row (unpadded)
+  // per-group block of g partials: D floats padded so that CPT consecutive-part blocks land
+  // on disjoint bank quads (part * GSTR mod 32 in steps of 4): 52 for D = 49, CPT = 8
+  static constexpr int GSTR = D == 49 ? 52 : ((D + 3) & ~3) + (((((D + 3) & ~3) / 4) % 2) ? 0 : 4);
   static constexpr int SPL = (KB + G - 1) / G;   // points whose prox scale a lane computes
   static constexpr int CPT = THREADS >= 8 * D ? 8 : THREADS >= 4 * D ? 4 : THREADS >= 2 * D ? 2 : 1;
   static_assert(SW % KB == 0, "segments tile the grid row");
   static_assert(D <= THREADS, "consensus needs one thread per coordinate");
 };
 
-using TileK7S21 = TileCfg<7, 21, 7>;   // configs 2, 3: 63 groups of 7 lanes, 16 warps
-using TileK5S11 = TileCfg<5, 11, 11>;  // config 0: 11 groups of 5 lanes, 2 warps
+// configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
+// SM hosts halves of two pixels and one half's barrier/exchange latency overlaps the other's FP work
+using TileK7S21 = TileCfg<7, 21, 7, 1>;    // single CTA per pixel (16 warps)
+using TileK7S21x2 = TileCfg<7, 21, 7, 2>;  // 2-CTA cluster per pixel (measured slower, kept)
+using TileK5S11 = TileCfg<5, 11, 11, 1>;   // config 0: 11 groups of 5 lanes, 2 warps
 
 template <class C>
 struct TileSmem {
   static constexpr int T = C::TH * C::TWS;            // one tile copy
-  static constexpr int NB = C::NGROUPS * C::G * C::KBP;  // norm transpose
-  static constexpr int RED = C::NGROUPS * C::G * C::KSP; // g / init partials
+  static constexpr int ROWS = C::NGC * C::G + 40;  // local groups + dummy rows for idle lanes
+  static constexpr int NB = ROWS * C::KBP;               // norm transpose
+  static constexpr int RED = (C::NGC + 8) * C::GSTR;     // g partials (+ dummy groups)
   static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
-                               C::NGROUPS * C::KBP /*w*/ + 64;
+                               C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/;
 };
 
 __device__ __forceinline__ float2 tf2(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float2 tsub2(float2 a, float2 b) {
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
@@ -85,18 +116,23 @@ struct TileCtx {
   float* T0;    // tile
   float* T1;    // tile shifted left by one column
   float* nbuf;  // [NGROUPS][G][KBP]
-  float* red;   // [NGROUPS][G][KSP]
+  float* red;   // [NGC + 8][GSTR] per-group g partials
   float2* c2;   // [D]
   float* z;     // [D]
   float* a0;    // [D]
   float* wbuf;  // [NGROUPS][KBP]
   int* flags;   // [4]
   float* scal;  // [32]
+  float* rx;    // [2][D + 8] cluster receive buffers (partials from the peer CTA)
   int tid, warp, lane, q, dr, base;
+  int grow0;    // first transpose/partial row of the lane's group (dummy rows if idle)
   bool active;  // lane belongs to a real group
   int gr, gc0;  // grid row and first grid column of the lane's segment
 
-  __device__ void carve(float* smem) {
+  int rank, nloc;  // CTA rank in the cluster, real groups held by this CTA
+  int xpar = 0;    // cluster exchange parity (double-buffered receive buffers)
+  int dbg_it = 0;  // debug phase-profile sweep counter
+  __device__ void carve(float* smem, int cta_rank) {
     T0 = smem;
     T1 = T0 + TileSmem<C>::T;
     nbuf = T1 + TileSmem<C>::T;
@@ -107,14 +143,19 @@ struct TileCtx {
     wbuf = a0 + C::D;
     flags = reinterpret_cast<int*>(wbuf + C::NGROUPS * C::KBP);
     scal = reinterpret_cast<float*>(flags + 8);
+    rx = scal + 32;
     tid = threadIdx.x;
     warp = tid >> 5;
     lane = tid & 31;
     const int ql = lane / C::G;
     dr = lane - ql * C::G;
     base = ql * C::G;
-    q = warp * C::GPW + ql;
-    active = ql < C::GPW && q < C::NGROUPS;
+    rank = cta_rank;
+    const int lq = warp * C::GPW + ql;  // local group
+    q = rank * C::NGC + lq;             // global group
+    nloc = min(C::NGC, C::NGROUPS - rank * C::NGC);
+    active = ql < C::GPW && lq < nloc;
+    grow0 = active ? lq * C::G : C::NGC * C::G + base;  // idle lanes: private dummy rows
     const int qq = active ? q : 0;
     gr = qq / C::NBLK;
     gc0 = (qq % C::NBLK) * C::KB;
@@ -125,23 +166,30 @@ struct TileCtx {
 // v[m] = this lane's partial for point m (m < KB); returns, for the SPL points m = dr + i*G
 // this lane owns, the group totals.  Fixed summation order (lanes 0..G-1).
 template <class C>
+__device__ __forceinline__ float tree_sum_col(const float* col, int stride) {
+  float v[C::G];
+#pragma unroll
+  for (int r = 0; r < C::G; ++r) v[r] = col[r * stride];
+#pragma unroll
+  for (int w = 1; w < C::G; w <<= 1)
+#pragma unroll
+    for (int r = 0; r + w < C::G; r += 2 * w) v[r] += v[r + w];
+  return v[0];
+}
+
+template <class C>
 __device__ __forceinline__ void group_point_totals(TileCtx<C>& X, const float (&v)[C::KB],
                                                    float (&tot)[C::SPL]) {
-  float* row = X.nbuf + (X.q * C::G + X.dr) * C::KBP;
-  if (X.active)
+  float* row = X.nbuf + (X.grow0 + X.dr) * C::KBP;
 #pragma unroll
-    for (int m = 0; m < C::KB; ++m) row[m] = v[m];
+  for (int m = 0; m < C::KB; ++m) row[m] = v[m];
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < C::SPL; ++i) {
     const int m = X.dr + i * C::G;
-    float t = 0.0f;
-    if (X.active && m < C::KB) {
-      const float* col = X.nbuf + X.q * C::G * C::KBP + m;
-#pragma unroll
-      for (int r = 0; r < C::G; ++r) t += col[r * C::KBP];
-    }
-    tot[i] = t;
+    tot[i] = (C::SPL == 1 || m < C::KB)
+                 ? tree_sum_col<C>(X.nbuf + X.grow0 * C::KBP + (m < C::KB ? m : 0), C::KBP)
+                 : 0.0f;
   }
   __syncwarp();
 }
@@ -161,39 +209,98 @@ __device__ __forceinline__ void group_broadcast(const TileCtx<C>& X, const float
 }
 
 // Sum the per-lane coordinate partials v[dc] (coordinate j = dr*KS + dc) over all groups:
-// lanes write red[q][dr][dc]; after a barrier CPT threads per coordinate sum groups in a
-// fixed order and `finish(j, total)` runs on one thread per coordinate.  Ends with a barrier.
+// lanes write red[lq][dr][dc]; after a barrier CPT threads per coordinate sum this CTA's
+// groups in a fixed order.  With a 2-CTA cluster the two partials are exchanged through
+// distributed shared memory (each CTA stores into the peer's receive buffer, one cluster
+// barrier) and combined as rank0 + rank1 in both CTAs, so both hold bitwise-identical
+// totals.  The local flag word flags[fslot] travels with the partials (OR-combined).
+// `finish(j, total)` runs on one thread per coordinate.  Ends with a CTA barrier.
 template <class C, class Finish>
 __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&v)[C::KS],
-                                                   Finish finish) {
-  if (X.active) {
-    float* row = X.red + (X.q * C::G + X.dr) * C::KSP;
+                                                   int fslot, Finish finish) {
+  {
+    float* row = X.red + (X.grow0 / C::G) * C::GSTR + X.dr * C::KS;  // idle lanes: dummy groups
 #pragma unroll
     for (int dc = 0; dc < C::KS; ++dc) row[dc] = v[dc];
   }
   __syncthreads();
+  PHASE(6);
   const int j = X.tid / C::CPT, part = X.tid % C::CPT;
   float s = 0.0f;
   if (j < C::D) {
-    const int jr = j / C::KS, jc = j - jr * C::KS;
-    const float* col = X.red + jr * C::KSP + jc;
-    for (int g = part; g < C::NGROUPS; g += C::CPT) s += col[g * C::G * C::KSP];
+    const float* col = X.red + part * C::GSTR + j;
+    // all loads first (independent), then a fixed-order pairwise tree
+    constexpr int NPER = (C::NGC + C::CPT - 1) / C::CPT;
+    float v[NPER];
+#pragma unroll
+    for (int i = 0; i < NPER; ++i)
+      v[i] = (part + i * C::CPT < X.nloc) ? col[i * C::CPT * C::GSTR] : 0.0f;
+#pragma unroll
+    for (int w = 1; w < NPER; w <<= 1)
+#pragma unroll
+      for (int i = 0; i + w < NPER; i += 2 * w) v[i] += v[i + w];
+    s = v[0];
   }
+  PHASE(7);
 #pragma unroll
   for (int o = 1; o < C::CPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  PHASE(8);
+  if constexpr (C::CL == 2) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    float* peer_rx = cl.map_shared_rank(X.rx, X.rank ^ 1) + X.xpar * (C::D + 8);
+    if (j < C::D && part == 0) peer_rx[j] = s;
+    if (X.tid == 0) reinterpret_cast<int*>(peer_rx)[C::D] = X.flags[fslot];
+    cl.sync();
+    const float* own_rx = X.rx + X.xpar * (C::D + 8);
+    if (j < C::D && part == 0) {
+      const float o = own_rx[j];
+      s = X.rank == 0 ? s + o : o + s;
+    }
+    if (X.tid == 0) {
+      const int pf = reinterpret_cast<const int*>(own_rx)[C::D];
+      if (pf) atomicOr(&X.flags[fslot], pf);
+    }
+    X.xpar ^= 1;
+  }
   if (j < C::D && part == 0) finish(j, s);
+  PHASE(9);
   __syncthreads();
+  PHASE(10);
+}
+
+// Cluster-wide sum of one scalar per lane (fixed order: warp tree, warps, rank0 + rank1).
+template <class C>
+__device__ __forceinline__ float cluster_sum_scalar(TileCtx<C>& X, float v) {
+  v = warp_sum(v);
+  if (X.lane == 0) X.scal[X.warp] = v;
+  __syncthreads();
+  float t = 0.0f;
+#pragma unroll
+  for (int w = 0; w < C::WARPS; ++w) t += X.scal[w];
+  if constexpr (C::CL == 2) {
+    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+    float* peer_rx = cl.map_shared_rank(X.rx, X.rank ^ 1) + X.xpar * (C::D + 8);
+    if (X.tid == 0) peer_rx[C::D + 1] = t;
+    cl.sync();
+    const float o = X.rx[X.xpar * (C::D + 8) + C::D + 1];
+    t = X.rank == 0 ? t + o : o + t;
+    X.xpar ^= 1;
+  }
+  __syncthreads();
+  return t;
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::CL)
 nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
                  int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
                  int* work_counter, int chunk, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   TileCtx<C> X;
-  X.carve(smem);
-  __shared__ int next_chunk;
+  int crank = 0;
+  if constexpr (C::CL == 2) crank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
+  X.carve(smem, crank);
+  (void)work_counter;
   constexpr int hs = C::SW / 2;
   constexpr int center = C::D / 2;
   const int64_t plane = out_rows * cols;
@@ -209,12 +316,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   for (int e = X.tid; e < 2 * TileSmem<C>::T; e += C::THREADS) X.T0[e] = 0.0f;
   __syncthreads();
 
-  for (;;) {
-    if (X.tid == 0) next_chunk = atomicAdd(work_counter, 1);
-    __syncthreads();
-    const int64_t ch = next_chunk;
-    __syncthreads();
-    if (ch >= nchunks) break;
+  // static round-robin over pixel chunks per cluster (both CTAs of a cluster walk the same
+  // pixels; work per chunk is uniform up to the clipped image border)
+  const int64_t cid = blockIdx.x / C::CL, ncl = gridDim.x / C::CL;
+  for (int64_t ch = cid; ch < nchunks; ch += ncl) {
     const int64_t pix_end = (ch + 1) * chunk < plane ? (ch + 1) * chunk : plane;
     for (int64_t pix = ch * chunk; pix < pix_end; ++pix) {
       const int64_t r = out_row0 + pix / cols, c = pix % cols;
@@ -245,6 +350,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       if (X.tid == 0) {
         X.flags[0] = 0;
         X.flags[1] = 0;
+        X.flags[2] = 0;
       }
       // ---- segment registers
       Seg<C> S;
@@ -307,16 +413,11 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         float wsum = 0.0f;
 #pragma unroll
         for (int i = 0; i < C::SPL; ++i) wsum += wown[i];
-        wsum = warp_sum(X.active ? wsum : 0.0f);
-        if (X.lane == 0) X.scal[X.warp] = wsum;
-        __syncthreads();
-        float W = 0.0f;
-#pragma unroll
-        for (int w = 0; w < C::WARPS; ++w) W += X.scal[w];
+        const float W = cluster_sum_scalar<C>(X, X.active ? wsum : 0.0f);
         const bool ratio = P.nlm_ratio != 0;
         float coef[C::KB];
 #pragma unroll
-        for (int m = 0; m < C::KB; ++m) coef[m] = ratio ? wall[m] : wall[m] / W;
+        for (int m = 0; m < C::KB; ++m) coef[m] = ratio ? wall[m] : wall[m] / W;  // points*(w/sum w)
         float v[C::KS];
 #pragma unroll
         for (int dc = 0; dc < C::KS; ++dc) {
@@ -328,7 +429,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           if (C::ODD) t = fmaf(coef[C::KB - 1], S.single(dc), t);
           v[dc] = X.active ? t : 0.0f;
         }
-        reduce_coordinates<C>(X, v, [&](int j, float tsum) { X.z[j] = ratio ? tsum / W : tsum; });
+        reduce_coordinates<C>(X, v, 2, [&](int j, float tsum) { X.z[j] = ratio ? tsum / W : tsum; });
       } else {
         if (X.tid < C::D) {
           const int jr = X.tid / C::KS, jc = X.tid - jr * C::KS;
@@ -359,6 +460,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         if (X.tid < C::D) X.c2[X.tid] = tf2(X.z[X.tid]);
         __syncthreads();
         for (int t = 1; t <= P.iters; ++t) {
+          PHASE(0);
           // (U) p' = s p + (c - a); per-point norm partials
           float nr[C::KB];
           {
@@ -388,24 +490,25 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
             }
           }
           // (R) group totals -> prox scales -> broadcast
+          PHASE(1);
           float tot[C::SPL], sown[C::SPL];
           group_point_totals<C>(X, nr, tot);
-          bool ok = true, one = true;
+          PHASE(2);
+          int fbits = 0;
 #pragma unroll
           for (int i = 0; i < C::SPL; ++i) {
-            const int m = X.dr + i * C::G;
-            const bool rm = is_real(m);
-            float s = 0.0f;
-            if (lam_own[i] != 0.0f) s = fminf(1.0f, lam_own[i] * rsqrtf(tot[i]));
+            const float lam = lam_own[i];
+            const float s = lam != 0.0f ? fminf(1.0f, lam * rsqrt_ftz(tot[i])) : 0.0f;
             sown[i] = s;
-            ok &= isfinite(tot[i]) || !rm;
-            one &= !rm || s == 1.0f;
+            fbits |= (lam != 0.0f && !isfinite(tot[i])) ? 1 : 0;
+            if (static_eq) fbits |= (is_real(X.dr + i * C::G) && s != 1.0f) ? 2 : 0;
           }
           float sall[C::KB];
           group_broadcast<C>(X, sown, sall);
 #pragma unroll
           for (int qq = 0; qq < C::KP; ++qq) s2[qq] = make_float2(sall[2 * qq], sall[2 * qq + 1]);
           if (C::ODD) s1 = sall[C::KB - 1];
+          PHASE(3);
           // (G) g partials per coordinate
           float v[C::KS];
 #pragma unroll
@@ -417,34 +520,39 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
             if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
             v[dc] = X.active ? tsum : 0.0f;
           }
-          const int wbad = __any_sync(0xffffffffu, !ok);
-          const int wnot1 = __any_sync(0xffffffffu, !one);
-          if (X.lane == 0 && (wbad | wnot1)) atomicOr(&X.flags[t & 1], (wbad ? 1 : 0) | (wnot1 ? 2 : 0));
+          fbits = __reduce_or_sync(0xffffffffu, fbits);
+          if (X.lane == 0 && fbits) atomicOr(&X.flags[t & 1], fbits);
+          PHASE(4);
           // consensus z_t = P_C(z - g/n), c = 2 z_t - z  (admm.hpp:59-65 in p-form)
-          reduce_coordinates<C>(X, v, [&](int j, float gsum) {
+          reduce_coordinates<C>(X, v, t & 1, [&](int j, float gsum) {
             const float zo = X.z[j];
             const float zn = clamp_box(fmaf(-gsum, inv_n, zo), P.range);
             int f = isfinite(zn) ? 0 : 4;
-            f |= (zn != X.a0[j]) ? 8 : 0;
+            if (static_eq) f |= (zn != X.a0[j]) ? 8 : 0;  // exact-stop test only if possible
             X.z[j] = zn;
             X.c2[j] = tf2(2.0f * zn - zo);
-            if (f) atomicOr(&X.flags[t & 1], f);
+            if (f) atomicOr(&X.flags[t & 1], f);  // rare: non-finite, or a constant footprint
             if (j == 0) X.flags[(t + 1) & 1] = 0;  // all reads of sweep t-1's word are done
           });
           const int fl = X.flags[t & 1];
+          PHASE(5);
+#ifdef NLEM_PHASE_PROFILE
+          ++X.dbg_it;
+#endif
           if (fl & (4 | 1)) {
             fail_iter = (fl & 4) || t == 1 ? t : t - 1;
             fail_kind = NLEM_FAIL_ADMM_ITERATE;
             break;
           }
-          if (frames && X.tid == 0) frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
+          if (frames && X.tid == 0 && X.rank == 0)
+            frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
           if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
             iters = t;
             break;
           }
         }
       }
-      if (X.tid == 0) {
+      if (X.tid == 0 && X.rank == 0) {
         if (fail_iter >= 0) {
           record_failure(fail, r * cols + c, fail_iter, fail_kind);
         } else {
@@ -471,25 +579,48 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
   const int64_t pixels = L.out_rows * L.cols;
-  const int64_t ctas = int64_t(device_caps().sms) * std::max(per_sm, 1);
-  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (ctas * 4))));
-  int* counter = nullptr;
-  e = cudaMallocAsync(&counter, sizeof(int), stream);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  cfg.blockDim = dim3(C::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  int64_t clusters = 1;
+  if constexpr (C::CL > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = C::CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cfg.gridDim = dim3(C::CL * 148);
+    int ncl = 0;
+    e = cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg);
+    if (e != cudaSuccess) return e;
+    clusters = std::max(ncl, 1);
+  } else {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
+    clusters = int64_t(device_caps().sms) * std::max(per_sm, 1);
+  }
+  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (clusters * 4))));
+  clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, (pixels + chunk - 1) / chunk));
+  cfg.gridDim = dim3(static_cast<unsigned>(clusters * C::CL));
+  e = cudaLaunchKernelEx(&cfg, kfn, L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P,
+                         L.out, L.frames, static_cast<int*>(nullptr), chunk, L.fail);
   if (e != cudaSuccess) return e;
-  cudaMemsetAsync(counter, 0, sizeof(int), stream);
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ctas, (pixels + chunk - 1) / chunk));
-  kfn<<<static_cast<unsigned>(grid), C::THREADS, smem, stream>>>(
-      L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out, L.frames, counter,
-      chunk, L.fail);
-  e = cudaGetLastError();
-  cudaFreeAsync(counter, stream);
-  return e;
+  return cudaGetLastError();
 }
 
 }  // namespace
+
+#ifdef NLEM_PHASE_PROFILE
+}  // namespace nlemk
+extern "C" int nlem_debug_phase_times(long long* out /* [2][64][16] */) {
+  return cudaMemcpyFromSymbol(out, nlemk::g_phase, sizeof(nlemk::g_phase)) == cudaSuccess ? 0 : 1;
+}
+namespace nlemk {
+#endif
 
 bool nlem_tile_supported(const NlemLaunch& L) {
   if (L.P.solver == NLEM_SOLVER_IRLS) return false;

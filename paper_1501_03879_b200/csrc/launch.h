@@ -86,6 +86,8 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream);
 // shape is not covered (the caller then uses the generic kernel).
 bool admm_fast_supported(const AdmmLaunch& L);
 cudaError_t launch_admm_fast(const AdmmLaunch& L, cudaStream_t stream);
+bool nlem_seg2_supported(const NlemLaunch& L);
+cudaError_t launch_nlem_seg2(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_fast_supported(const NlemLaunch& L);

@@ -1,0 +1,96 @@
+"""Secondary measurements (not the driver's headline line): BASELINE config 1 (batched
+standalone EM-ADMM, 65,536 problems, n=441, d=49, T=50, box and unconstrained, problems/s)
+and config 2 (NLEM 512^2, Mpixels/s), device-resident, CUDA-event timed, L2 flushed.
+Prints one JSON object."""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_1501_03879_b200 as nb
+from paper_1501_03879_b200 import _lib as L, synth
+
+PEAK = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def timed(fn, reps, flush):
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def measure(problems=65536, reps=3):
+    class A:
+        pass
+    a = A()
+    a.problems, a.reps = problems, reps
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+    res = {}
+    # ---- config 1
+    B, n, d, T = a.problems, 441, 49, 50
+    t0 = time.time()
+    P = torch.empty((B, n, d), device="cuda")
+    W = torch.empty((B, n), device="cuda")
+    step = 4096
+    for b0 in range(0, B, step):
+        nb_ = min(step, B - b0)
+        pts, w = synth.point_sets(nb_, first=b0)
+        P[b0:b0 + nb_].copy_(torch.from_numpy(pts))
+        W[b0:b0 + nb_].copy_(torch.from_numpy(w))
+    gen_s = time.time() - t0
+    z = torch.empty((B, d), device="cuda")
+    cfg = L.AdmmConfigC()
+    cfg.mu, cfg.max_iter, cfg.tol_primal = 1.0, T, 0.0
+    lib = L.load()
+    import ctypes as C
+    for name, box in (("box", nb.BoxConstraint.interval(0.0, 255.0)),
+                      ("unconstrained", nb.BoxConstraint.unconstrained())):
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+        def run():
+            lib.nlem_admm_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d, None,
+                                  box.c(), cfg, C.c_void_p(z.data_ptr()), None, None, None, None,
+                                  None, st)
+        ms = timed(run, a.reps, flush)
+        flops = 12 * d * T * n * B
+        res[f"config1_{name}"] = {"problems_per_s": B / (ms / 1e3), "ms": ms,
+                                  "tflops_algorithmic": flops / (ms / 1e3) / 1e12,
+                                  "frac_fp32_peak": flops / (ms / 1e3) / 1e12 / PEAK}
+    res["config1_generation_s"] = gen_s
+    del P, W
+    # ---- config 2
+    clean, noisy = synth.config_image(2)
+    p = nb.NlemParams(search=21, patch=7, h=10 * 20.0 * math.sqrt(49), sigma=20.0, solver_iters=10,
+                      mu=1.0, init_mode="nlm")
+    X = torch.from_numpy(noisy).cuda()
+    ms = timed(lambda: nb.nlem_denoise(X, p), a.reps, flush)
+    res["config2"] = {"mpix_per_s": 512 * 512 / (ms / 1e3) / 1e6, "ms": ms}
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--problems", type=int, default=65536)
+    ap.add_argument("--reps", type=int, default=3)
+    a = ap.parse_args()
+    print(json.dumps(measure(a.problems, a.reps)))
+
+
+if __name__ == "__main__":
+    main()

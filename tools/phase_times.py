@@ -1,0 +1,46 @@
+"""Per-phase cycle counts of the NLEM tile kernel sweep (debug build with NLEM_PHASE_PROFILE).
+usage: python tools/phase_times.py   (builds _lib/libnlem_b200_prof.so first)"""
+import ctypes as C
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+from paper_1501_03879_b200 import build as B
+
+so = B.build(force=True, variant="prof")
+import paper_1501_03879_b200._lib as L
+
+L.SO_PATH = so
+import paper_1501_03879_b200 as nb
+import torch
+from paper_1501_03879_b200 import synth
+
+_, noisy = synth.noisy_image(512, 512, 40, 30, 30.0)
+p = nb.NlemParams(search=21, patch=7, h=10 * 30.0 * math.sqrt(49), solver_iters=10, mu=1.0,
+                  init_mode="nlm")
+X = torch.from_numpy(noisy).cuda()
+out = nb.nlem_denoise_rows(X[200:280], 200, 512, 512, 213, 16, p)
+torch.cuda.synchronize()
+buf = np.zeros((2, 64, 16), np.int64)
+lib = L.load(build_if_missing=False)
+assert lib.nlem_debug_phase_times(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
+names = ["update+norm", "norm-exchange", "s+bcast", "g+flags", "barrier+consensus+barrier", "->next",
+         "  red write+barrier1", "  consensus loads+tree", "  xor shuffles", "  finish", "  barrier2"]
+for w in range(2):
+    d = buf[w]
+    valid = [i for i in range(64) if d[i, 0] and d[i, 5]]
+    rows = []
+    for i in valid:
+        seg = [d[i, k + 1] - d[i, k] for k in range(5)]
+        nxt = d[i + 1, 0] - d[i, 5] if i + 1 in valid else 0
+        sub = [d[i, 6] - d[i, 4], d[i, 7] - d[i, 6], d[i, 8] - d[i, 7], d[i, 9] - d[i, 8],
+               d[i, 10] - d[i, 9]]
+        rows.append(seg + [nxt] + sub)
+    a = np.array(rows[2:])  # skip warm-up sweeps
+    print(f"warp {'0' if w == 0 else 'last'}: sweeps={len(a)}")
+    for k, n in enumerate(names):
+        print(f"   {n:28s} mean {a[:, k].mean():8.1f}  median {np.median(a[:, k]):8.1f}")
+    print(f"   total per sweep (median)     {np.median(a[:, :5].sum(1) + a[:, 5]):8.1f}")
