@@ -49,7 +49,9 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     for src in sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
         if src.endswith(".cu"):
-            extra = ["-DNLEM_PHASE_PROFILE"] if variant == "prof" else []
+            extra = ["-DNLEM_PHASE_PROFILE"] if variant.startswith("prof") else []
+            if variant == "prof_cl2":
+                extra.append("-DNLEM_TILE_CL=2")
             cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++20", "-fPIC", "-c", src, "-o", obj]

@@ -69,8 +69,13 @@ struct TileCfg {
 
 // configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
 // SM hosts halves of two pixels and one half's barrier/exchange latency overlaps the other's FP work
-using TileK7S21 = TileCfg<7, 21, 7, 1>;    // single CTA per pixel (16 warps)
-using TileK7S21x2 = TileCfg<7, 21, 7, 2>;  // 2-CTA cluster per pixel (measured slower, kept)
+#ifndef NLEM_TILE_CL
+#define NLEM_TILE_CL 1
+#endif
+// 1: one CTA per pixel (16 warps) — production.  2: pixel split over a 2-CTA cluster with a
+// DSMEM + mbarrier exchange per sweep — experimental: measured slower, the per-sweep exchange
+// waits ~1.2-1.7k cycles on skew between the two SMs (profiles/r1_tile_phase_times.txt)
+using TileK7S21 = TileCfg<7, 21, 7, NLEM_TILE_CL>;
 using TileK5S11 = TileCfg<5, 11, 11, 1>;   // config 0: 11 groups of 5 lanes, 2 warps
 
 template <class C>
@@ -80,10 +85,41 @@ struct TileSmem {
   static constexpr int NB = ROWS * C::KBP;               // norm transpose
   static constexpr int RED = (C::NGC + 8) * C::GSTR;     // g partials (+ dummy groups)
   static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
-                               C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/;
+                               C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
+                               4 /*mbarrier*/;
 };
 
 __device__ __forceinline__ float2 tf2(float x) { return make_float2(x, x); }
+
+// --- cluster one-way exchange: DSMEM store + remote mbarrier arrive (release.cluster), local
+// parity wait (acquire.cluster).  Cheaper than a full cluster barrier: a consumer waits only
+// for the peer's producers, not for every thread of both CTAs.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t local, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+constexpr int kExchArrivals = 50;  // 49 coordinate producers + thread 0 (flags / scalar)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -124,6 +160,7 @@ struct TileCtx {
   int* flags;   // [4]
   float* scal;  // [32]
   float* rx;    // [2][D + 8] cluster receive buffers (partials from the peer CTA)
+  unsigned long long* mbar;  // cluster exchange mbarrier (arrivals from the peer CTA)
   int tid, warp, lane, q, dr, base;
   int grow0;    // first transpose/partial row of the lane's group (dummy rows if idle)
   bool active;  // lane belongs to a real group
@@ -144,6 +181,8 @@ struct TileCtx {
     flags = reinterpret_cast<int*>(wbuf + C::NGROUPS * C::KBP);
     scal = reinterpret_cast<float*>(flags + 8);
     rx = scal + 32;
+    mbar = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<uintptr_t>(rx + 2 * (C::D + 8) + 1) & ~uintptr_t(7));
     tid = threadIdx.x;
     warp = tid >> 5;
     lane = tid & 31;
@@ -246,11 +285,18 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
   for (int o = 1; o < C::CPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   PHASE(8);
   if constexpr (C::CL == 2) {
-    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-    float* peer_rx = cl.map_shared_rank(X.rx, X.rank ^ 1) + X.xpar * (C::D + 8);
-    if (j < C::D && part == 0) peer_rx[j] = s;
-    if (X.tid == 0) reinterpret_cast<int*>(peer_rx)[C::D] = X.flags[fslot];
-    cl.sync();
+    const uint32_t peer = static_cast<uint32_t>(X.rank ^ 1);
+    const uint32_t rx_peer = mapa_peer(smem_u32(X.rx + X.xpar * (C::D + 8)), peer);
+    const uint32_t mb_peer = mapa_peer(smem_u32(X.mbar), peer);
+    if (j < C::D && part == 0) {
+      st_cluster_f32(rx_peer + 4u * j, s);
+      mbar_arrive_remote(mb_peer);
+    }
+    if (X.tid == 0) {
+      st_cluster_u32(rx_peer + 4u * C::D, static_cast<uint32_t>(X.flags[fslot]));
+      mbar_arrive_remote(mb_peer);
+    }
+    if ((j < C::D && part == 0) || X.tid == 0) mbar_wait_parity(smem_u32(X.mbar), X.xpar);
     const float* own_rx = X.rx + X.xpar * (C::D + 8);
     if (j < C::D && part == 0) {
       const float o = own_rx[j];
@@ -262,6 +308,7 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
     }
     X.xpar ^= 1;
   }
+  PHASE(11);
   if (j < C::D && part == 0) finish(j, s);
   PHASE(9);
   __syncthreads();
@@ -278,13 +325,21 @@ __device__ __forceinline__ float cluster_sum_scalar(TileCtx<C>& X, float v) {
 #pragma unroll
   for (int w = 0; w < C::WARPS; ++w) t += X.scal[w];
   if constexpr (C::CL == 2) {
-    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-    float* peer_rx = cl.map_shared_rank(X.rx, X.rank ^ 1) + X.xpar * (C::D + 8);
-    if (X.tid == 0) peer_rx[C::D + 1] = t;
-    cl.sync();
-    const float o = X.rx[X.xpar * (C::D + 8) + C::D + 1];
-    t = X.rank == 0 ? t + o : o + t;
+    // same 50-arrival protocol as reduce_coordinates: threads 0..48 arrive, thread 0 twice
+    const uint32_t peer = static_cast<uint32_t>(X.rank ^ 1);
+    const uint32_t rx_peer = mapa_peer(smem_u32(X.rx + X.xpar * (C::D + 8)), peer);
+    const uint32_t mb_peer = mapa_peer(smem_u32(X.mbar), peer);
+    if (X.tid == 0) st_cluster_f32(rx_peer + 4u * (C::D + 1), t);
+    if (X.tid < kExchArrivals - 1) mbar_arrive_remote(mb_peer);
+    if (X.tid == 0) mbar_arrive_remote(mb_peer);
+    if (X.tid == 0) {
+      mbar_wait_parity(smem_u32(X.mbar), X.xpar);
+      const float o = X.rx[X.xpar * (C::D + 8) + C::D + 1];
+      X.scal[31] = X.rank == 0 ? t + o : o + t;
+    }
     X.xpar ^= 1;
+    __syncthreads();
+    t = X.scal[31];
   }
   __syncthreads();
   return t;
@@ -314,6 +369,14 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   const bool useT1E = !even, useT1O = even;
   // zero the tile slack columns once
   for (int e = X.tid; e < 2 * TileSmem<C>::T; e += C::THREADS) X.T0[e] = 0.0f;
+  if constexpr (C::CL == 2) {
+    if (X.tid == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(X.mbar)),
+                   "r"(kExchArrivals));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    cooperative_groups::this_cluster().sync();  // peer's mbarrier initialised before use
+  }
   __syncthreads();
 
   // static round-robin over pixel chunks per cluster (both CTAs of a cluster walk the same
@@ -568,6 +631,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       __syncthreads();
     }
   }
+  // no CTA may exit while its peer can still store into its shared memory
+  if constexpr (C::CL == 2) cooperative_groups::this_cluster().sync();
 }
 
 namespace {

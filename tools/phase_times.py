@@ -10,7 +10,7 @@ import numpy as np
 
 from paper_1501_03879_b200 import build as B
 
-so = B.build(force=True, variant="prof")
+so = B.build(force=True, variant=os.environ.get("PROF_VARIANT", "prof"))
 import paper_1501_03879_b200._lib as L
 
 L.SO_PATH = so
@@ -28,7 +28,8 @@ buf = np.zeros((2, 64, 16), np.int64)
 lib = L.load(build_if_missing=False)
 assert lib.nlem_debug_phase_times(buf.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
 names = ["update+norm", "norm-exchange", "s+bcast", "g+flags", "barrier+consensus+barrier", "->next",
-         "  red write+barrier1", "  consensus loads+tree", "  xor shuffles", "  finish", "  barrier2"]
+         "  red write+barrier1", "  consensus loads+tree", "  xor shuffles", "  (cluster xchg)+finish", "  barrier2",
+         "  cluster exchange only"]
 for w in range(2):
     d = buf[w]
     valid = [i for i in range(64) if d[i, 0] and d[i, 5]]
@@ -37,7 +38,7 @@ for w in range(2):
         seg = [d[i, k + 1] - d[i, k] for k in range(5)]
         nxt = d[i + 1, 0] - d[i, 5] if i + 1 in valid else 0
         sub = [d[i, 6] - d[i, 4], d[i, 7] - d[i, 6], d[i, 8] - d[i, 7], d[i, 9] - d[i, 8],
-               d[i, 10] - d[i, 9]]
+               d[i, 10] - d[i, 9], d[i, 11] - d[i, 8]]
         rows.append(seg + [nxt] + sub)
     a = np.array(rows[2:])  # skip warm-up sweeps
     print(f"warp {'0' if w == 0 else 'last'}: sweeps={len(a)}")
