@@ -119,7 +119,15 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t addr, uint32_t parity)
       "r"(parity)
       : "memory");
 }
-constexpr int kExchArrivals = 50;  // 49 coordinate producers + thread 0 (flags / scalar)
+constexpr int kExchArrivals = 50;
+
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}  // 49 coordinate producers + thread 0 (flags / scalar)
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -315,6 +323,59 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
   PHASE(10);
 }
 
+// IRLS consensus (CL == 1): lanes write their num partials v[dc] (coordinate j = dr*KS + dc)
+// and one lane per group writes the group's sum beta and sum w*root into columns D and D+1 of
+// the group row (GSTR >= D + 2).  CPT threads per coordinate sum the 3 columns over groups in
+// a fixed order; finish(j, num, den, sur) runs on one thread per coordinate.
+template <class C, class Finish>
+__device__ __forceinline__ void irls_reduce(TileCtx<C>& X, const float (&v)[C::KS], float gden,
+                                            float gsur, Finish finish) {
+  static_assert(C::GSTR >= C::D + 2, "room for the den / surrogate columns");
+  {
+    float* row = X.red + (X.grow0 / C::G) * C::GSTR;
+#pragma unroll
+    for (int dc = 0; dc < C::KS; ++dc) row[X.dr * C::KS + dc] = v[dc];
+    if (X.dr == 0) {
+      row[C::D] = gden;
+      row[C::D + 1] = gsur;
+    }
+  }
+  __syncthreads();
+  const int j = X.tid / C::CPT, part = X.tid % C::CPT;
+  float sn = 0.0f, sd = 0.0f, ss = 0.0f;
+  if (j < C::D) {
+    constexpr int NPER = (C::NGC + C::CPT - 1) / C::CPT;
+    float a[NPER], b[NPER], c[NPER];
+#pragma unroll
+    for (int i = 0; i < NPER; ++i) {
+      const bool ok = part + i * C::CPT < X.nloc;
+      const float* g = X.red + (part + i * C::CPT) * C::GSTR;
+      a[i] = ok ? g[j] : 0.0f;
+      b[i] = ok ? g[C::D] : 0.0f;
+      c[i] = ok ? g[C::D + 1] : 0.0f;
+    }
+#pragma unroll
+    for (int w = 1; w < NPER; w <<= 1)
+#pragma unroll
+      for (int i = 0; i + w < NPER; i += 2 * w) {
+        a[i] += a[i + w];
+        b[i] += b[i + w];
+        c[i] += c[i + w];
+      }
+    sn = a[0];
+    sd = b[0];
+    ss = c[0];
+  }
+#pragma unroll
+  for (int o = 1; o < C::CPT; o <<= 1) {
+    sn += __shfl_xor_sync(0xffffffffu, sn, o);
+    sd += __shfl_xor_sync(0xffffffffu, sd, o);
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  }
+  if (j < C::D && part == 0) finish(j, sn, sd, ss);
+  __syncthreads();
+}
+
 // Cluster-wide sum of one scalar per lane (fixed order: warp tree, warps, rank0 + rank1).
 template <class C>
 __device__ __forceinline__ float cluster_sum_scalar(TileCtx<C>& X, float v) {
@@ -382,6 +443,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   // static round-robin over pixel chunks per cluster (both CTAs of a cluster walk the same
   // pixels; work per chunk is uniform up to the clipped image border)
   const int64_t cid = blockIdx.x / C::CL, ncl = gridDim.x / C::CL;
+  int64_t prefetched = -1;  // pixel whose tile is already in flight to smem
   for (int64_t ch = cid; ch < nchunks; ch += ncl) {
     const int64_t pix_end = (ch + 1) * chunk < plane ? (ch + 1) * chunk : plane;
     for (int64_t pix = ch * chunk; pix < pix_end; ++pix) {
@@ -392,13 +454,18 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       const int gc1w = cols - 1 - c < hs ? static_cast<int>(hs + (cols - 1 - c)) : C::SW - 1;
       const int n = (gr1 - gr0 + 1) * (gc1w - gc0w + 1);
       const float inv_n = 1.0f / static_cast<float>(n);
-      // ---- tile (and its one-column-shifted copy) from the padded band
-      const float* src = pad + (r - out_row0) * pad_cols + c;
-      for (int e = X.tid; e < C::TH * C::TH; e += C::THREADS) {
-        const int tr = e / C::TH, tc = e - tr * C::TH;
-        const float v = __ldg(src + tr * pad_cols + tc);
-        X.T0[tr * C::TWS + tc] = v;
-        if (tc > 0) X.T1[tr * C::TWS + tc - 1] = v;
+      // ---- tile (and its one-column-shifted copy) from the padded band; after the first
+      // pixel it was prefetched with cp.async during the previous pixel's sweeps
+      if (prefetched == pix) {
+        cp_async_wait_all();
+      } else {
+        const float* src = pad + (r - out_row0) * pad_cols + c;
+        for (int e = X.tid; e < C::TH * C::TH; e += C::THREADS) {
+          const int tr = e / C::TH, tc = e - tr * C::TH;
+          const float v = __ldg(src + tr * pad_cols + tc);
+          X.T0[tr * C::TWS + tc] = v;
+          if (tc > 0) X.T1[tr * C::TWS + tc - 1] = v;
+        }
       }
       __syncthreads();
       // footprint-constancy (all real patches equal <=> exact-stop candidate) and a0
@@ -471,7 +538,33 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       group_broadcast<C>(X, wown, wall);
       // ---- initial patch (nlem.cpp:13-18)
       const bool nlm_init = P.solver == NLEM_SOLVER_NLM_ONLY || P.init_mode == NLEM_INIT_NLM_PATCH;
-      if (nlm_init) {
+      bool init_done = false;
+      if constexpr (C::CL == 1) {
+        if (nlm_init) {
+          // sum_k w_k a_k / sum_k w_k with the weight sum riding along as an extra consensus
+          // column (one reduction, no separate W pass); algebraically the reference's
+          // points * (w / sum w) (types.hpp:73), exact for constant integer images
+          float v[C::KS];
+#pragma unroll
+          for (int dc = 0; dc < C::KS; ++dc) {
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 0; k < C::KP; ++k)
+              acc = tfma2(make_float2(wall[2 * k], wall[2 * k + 1]), S.pair(k, dc), acc);
+            float t = acc.x + acc.y;
+            if (C::ODD) t = fmaf(wall[C::KB - 1], S.single(dc), t);
+            v[dc] = X.active ? t : 0.0f;
+          }
+          float gw = 0.0f;
+#pragma unroll
+          for (int m = 0; m < C::KB; ++m) gw += wall[m];
+          irls_reduce<C>(X, v, X.active ? gw : 0.0f, 0.0f,
+                         [&](int j, float num, float den, float) { X.z[j] = num / den; });
+          init_done = true;
+        }
+      }
+      if (init_done) {
+      } else if (nlm_init) {
         // W = sum of weights (each point counted once by its owner lane)
         float wsum = 0.0f;
 #pragma unroll
@@ -501,7 +594,136 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         __syncthreads();
       }
 
+      // prefetch the next pixel's tile while this pixel's sweeps run (the tile is only read
+      // during the setup above, which ended with a barrier)
+      {
+        int64_t nxt = pix + 1;
+        if (nxt >= pix_end) nxt = (ch + ncl) * chunk < plane ? (ch + ncl) * chunk : -1;
+        if (nxt >= 0) {
+          const int64_t nr_ = out_row0 + nxt / cols, nc_ = nxt % cols;
+          const float* nsrc = pad + (nr_ - out_row0) * pad_cols + nc_;
+          for (int e = X.tid; e < C::TH * C::TH; e += C::THREADS) {
+            const int tr = e / C::TH, tc = e - tr * C::TH;
+            cp_async4(&X.T0[tr * C::TWS + tc], nsrc + tr * pad_cols + tc);
+            if (tc > 0) cp_async4(&X.T1[tr * C::TWS + tc - 1], nsrc + tr * pad_cols + tc);
+          }
+          asm volatile("cp.async.commit_group;" ::: "memory");
+          prefetched = nxt;
+        }
+      }
       int iters = P.iters, fail_iter = -1, fail_kind = 0;
+      if constexpr (C::CL == 1) {
+        if (P.solver == NLEM_SOLVER_IRLS) {
+          // ---- IRLS on the smooth surrogate (proj/include/nlem/irls.hpp:21-68): pass p
+          // evaluates at x_p: surrogate S(x_p) and beta_k = w_k / sqrt(||x_p - a_k||^2 + eps),
+          // then x_{p+1} = sum beta a / sum beta.  Pass 0 gives `previous`; pass t gives the
+          // iteration-t objective, the stop test and (if t < T) the next iterate.
+          float wown0 = wown[0];
+          float previous = 0.0f;
+          int stop_at = -1;
+          for (int pass = 0; pass <= P.iters; ++pass) {
+            float xv[C::KS];
+#pragma unroll
+            for (int dc = 0; dc < C::KS; ++dc) xv[dc] = X.z[X.dr * C::KS + dc];
+            float d2[C::KB];
+#pragma unroll
+            for (int k = 0; k < C::KP; ++k) {
+              float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) {
+                const float2 e = tsub2(S.pair(k, dc), tf2(xv[dc]));
+                acc = tfma2(e, e, acc);
+              }
+              d2[2 * k] = acc.x;
+              d2[2 * k + 1] = acc.y;
+            }
+            if (C::ODD) {
+              float acc = 0.0f;
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) {
+                const float e = S.single(dc) - xv[dc];
+                acc = fmaf(e, e, acc);
+              }
+              d2[C::KB - 1] = acc;
+            }
+            float tot[C::SPL];
+            group_point_totals<C>(X, d2, tot);
+            float bown[C::SPL], sown[C::SPL];
+#pragma unroll
+            for (int i = 0; i < C::SPL; ++i) {
+              const float w = i == 0 ? wown0 : wown[i];
+              const float root = sqrtf(tot[i] + P.epsilon);
+              bown[i] = w / root;   // irls.hpp:45-46
+              sown[i] = w * root;   // costs.hpp:24-33
+            }
+            float ball[C::KB], surall[C::KB];
+            group_broadcast<C>(X, bown, ball);
+            group_broadcast<C>(X, sown, surall);
+            float gden = 0.0f, gsur = 0.0f;
+#pragma unroll
+            for (int m = 0; m < C::KB; ++m) {
+              gden += ball[m];
+              gsur += surall[m];
+            }
+            float v[C::KS];
+#pragma unroll
+            for (int dc = 0; dc < C::KS; ++dc) {
+              float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int k = 0; k < C::KP; ++k)
+                acc = tfma2(make_float2(ball[2 * k], ball[2 * k + 1]), S.pair(k, dc), acc);
+              float t2 = acc.x + acc.y;
+              if (C::ODD) t2 = fmaf(ball[C::KB - 1], S.single(dc), t2);
+              v[dc] = X.active ? t2 : 0.0f;
+            }
+            if (!X.active) {
+              gden = 0.0f;
+              gsur = 0.0f;
+            }
+            if (X.tid == 0) X.flags[pass & 1] = 0;
+            __syncthreads();
+            irls_reduce<C>(X, v, gden, gsur, [&](int j, float num, float den, float sur) {
+              const float xo = X.z[j];
+              const float xn = num / den;
+              X.a0[j] = xo;  // keep x_pass (the iterate the stop test refers to)
+              X.z[j] = xn;
+              int f = isfinite(xn) ? 0 : 1;
+              if (j == 0) {
+                X.scal[16] = sur;
+                f |= isfinite(sur) ? 0 : 2;
+              }
+              if (f) atomicOr(&X.flags[pass & 1], f);
+            });
+            const int fl = X.flags[pass & 1];
+            const float current = X.scal[16];
+            if (fl & 2) {  // non-finite surrogate at x_pass (irls.hpp:39, :52)
+              fail_iter = pass;
+              fail_kind = NLEM_FAIL_IRLS_OBJECTIVE;
+              break;
+            }
+            if (pass >= 1) {
+              if (frames && X.tid == 0)
+                frames[static_cast<int64_t>(pass - 1) * plane + pix] = clamp_box(X.a0[center], P.range);
+              if (previous - current <= P.irls_tol * fabsf(previous)) {  // irls.hpp:58
+                stop_at = pass;
+                break;
+              }
+            }
+            previous = current;
+            if (pass < P.iters && (fl & 1)) {  // non-finite x_{pass+1} (irls.hpp:50)
+              fail_iter = pass + 1;
+              fail_kind = NLEM_FAIL_IRLS_ITERATE;
+              break;
+            }
+          }
+          // the minimiser is x at the stop pass (or x_T); X.a0 holds it, z holds x_{+1}
+          if (fail_iter < 0) {
+            iters = stop_at > 0 ? stop_at : P.iters;
+            if (X.tid < C::D) X.z[X.tid] = X.a0[X.tid];
+          }
+          __syncthreads();
+        }
+      }
       if (P.solver == NLEM_SOLVER_ADMM) {
         // ---- EM-ADMM sweeps in p-form (see solver_generic.cuh)
         float lam_own[C::SPL];
@@ -623,7 +845,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           if (P.solver != NLEM_SOLVER_ADMM) v = clamp_box(v, P.range);  // NlmOnly (nlem.cpp:26-31)
           out[pix] = v;
           if (frames) {
-            const int from = P.solver == NLEM_SOLVER_ADMM ? iters : 0;
+            const int from = P.solver == NLEM_SOLVER_NLM_ONLY ? 0 : iters;
             for (int t = from; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = v;
           }
         }
@@ -688,7 +910,7 @@ namespace nlemk {
 #endif
 
 bool nlem_tile_supported(const NlemLaunch& L) {
-  if (L.P.solver == NLEM_SOLVER_IRLS) return false;
+  if (L.P.solver == NLEM_SOLVER_IRLS && TileK7S21::CL != 1 && L.P.patch == 7) return false;
   return (L.P.patch == 7 && L.P.search == 21) || (L.P.patch == 5 && L.P.search == 11);
 }
 

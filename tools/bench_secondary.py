@@ -81,6 +81,25 @@ def measure(problems=65536, reps=3):
     X = torch.from_numpy(noisy).cuda()
     ms = timed(lambda: nb.nlem_denoise(X, p), a.reps, flush)
     res["config2"] = {"mpix_per_s": 512 * 512 / (ms / 1e3) / 1e6, "ms": ms}
+    # ---- config 4: convergence sweep, ADMM vs IRLS (eps=1e-4, fixed count), T = 1..100
+    sweep = {}
+    for sigma in (10.0, 20.0, 40.0, 60.0):
+        clean, noisy = synth.noisy_image(512, 512, 40, 30, sigma)
+        X = torch.from_numpy(noisy).cuda()
+        h = 10 * sigma * math.sqrt(49)
+        entry = {}
+        for solver, kw in (("admm", dict(mu=1.0)), ("irls", dict(epsilon=1e-4, irls_tol=-1.0))):
+            pr = nb.NlemParams(search=21, patch=7, h=h, sigma=sigma, solver=solver, solver_iters=100,
+                               init_mode="nlm", **kw)
+            ms = timed(lambda: nb.nlem_denoise_snapshots(X, pr), 1, flush)
+            fr = nb.nlem_denoise_snapshots(X, pr).cpu().numpy().astype(np.float64)
+            mse = ((fr - clean.astype(np.float64)[None]) ** 2).mean(axis=(1, 2))
+            psnr = 10 * np.log10(255.0 ** 2 / mse)
+            entry[solver] = {"ms_per_iteration": ms / 100,
+                             "psnr_db": {str(t): float(psnr[t - 1]) for t in (1, 2, 3, 4, 5, 10, 20, 50, 100)}}
+        entry["psnr_noisy_db"] = float(10 * np.log10(255.0 ** 2 / ((noisy.astype(np.float64) - clean) ** 2).mean()))
+        sweep[str(int(sigma))] = entry
+    res["config4"] = sweep
     return res
 
 
