@@ -360,6 +360,7 @@ def main():
         "gpu_launches": 2 * args.steps,
         "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
         "secondary": secondary,
+        "step_ms": [round(x, 2) for x in step_ms],
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
