@@ -187,6 +187,22 @@ nlem_status nlem_denoise_host(const float* noisy, int64_t rows, int64_t cols,
 nlem_status nlm_denoise(const float* noisy, int64_t rows, int64_t cols, const nlem_params* params,
                         float* out, nlem_failure* failure, void* stream);
 
+/* PSNR of every frame against `clean` (proj/include/nlem/psnr.hpp:12-24: peak 255, +inf when
+ * identical), reduced on the device in FP64: frames [nframes][count] and clean [count] are
+ * device buffers, psnr_out [nframes] is HOST memory (the call synchronizes `stream`).
+ * Lets config-4 style convergence sweeps skip the T x H x W frame download. */
+nlem_status nlem_frames_psnr(const float* frames, const float* clean, int64_t nframes,
+                             int64_t count, double* psnr_out, nlem_failure* failure, void* stream);
+
+/* Batched first-order optimality certificate (proj/include/nlem/diagnostics.hpp:22-55):
+ * residual_out[b] = max(0, ||g_b|| - sum of coincident weights) with active box faces
+ * absorbing blocked components; 0 certifies z_b optimal.  Device buffers; z must lie in the
+ * box (else the residual is NaN, where the reference throws). */
+nlem_status nlem_optimality_residual_batched(const float* points, const float* weights,
+                                             int64_t batch, int64_t n, int64_t d, nlem_box box,
+                                             const float* z, float* residual_out,
+                                             nlem_failure* failure, void* stream);
+
 /* Halo (rows) a band needs on each side: S/2 + k/2 (13 for S=21, k=7). */
 int64_t nlem_band_halo(const nlem_params* params);
 

@@ -53,7 +53,7 @@ EXPORTS = [
     "nlem_irls_batched_host", "nlem_denoise",
     "nlem_denoise_rows", "nlem_denoise_rows_host", "nlem_denoise_host", "nlm_denoise", "nlem_band_halo",
     "nlem_add_gaussian_noise", "nlem_synth_clean_image", "nlem_synth_noisy_image",
-    "nlem_synth_point_sets",
+    "nlem_synth_point_sets", "nlem_frames_psnr", "nlem_optimality_residual_batched",
 ]
 
 _lib = None
@@ -98,6 +98,9 @@ def load(build_if_missing: bool = True):
                                     C.POINTER(Failure), C.c_int32]
     L.nlm_denoise.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(ParamsC), vp,
                               C.POINTER(Failure), vp]
+    L.nlem_frames_psnr.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, C.POINTER(Failure), vp]
+    L.nlem_optimality_residual_batched.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int64, Box, vp,
+                                                   vp, C.POINTER(Failure), vp]
     L.nlem_add_gaussian_noise.argtypes = [vp, C.c_int64, C.c_double, C.c_uint64, vp]
     L.nlem_synth_clean_image.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_uint64, vp]
     L.nlem_synth_noisy_image.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double,

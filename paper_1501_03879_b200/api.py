@@ -391,3 +391,42 @@ def nlem_denoise_rows(noisy_rows, in_row0: int, rows: int, cols: int, out_row0: 
                                         C.byref(f), _stream(dev))
     _raise(st, f)
     return (out, fr) if frames else out
+
+
+# ---- SURVEY §8f "next" rows: device-side quality / certificate reductions -----------------
+def frames_psnr(frames, clean) -> np.ndarray:
+    """PSNR of every snapshot frame vs `clean` (psnr.hpp:12-24), reduced on the GPU in FP64."""
+    torch = _torch()
+    F = _dev(frames)
+    Cl = _dev(clean, device=F.device)
+    T = F.shape[0]
+    count = Cl.numel()
+    if F.numel() != T * count:
+        raise InvalidArgument("frames and clean image sizes differ")
+    out = np.empty(T, np.float64)
+    f = L.Failure()
+    with torch.cuda.device(F.device):
+        st = L.load().nlem_frames_psnr(_ptr(F), _ptr(Cl), T, count, out.ctypes.data, C.byref(f),
+                                       _stream(F.device))
+    _raise(st, f)
+    return out
+
+
+def optimality_residual(points, weights, z, box: BoxConstraint | None = None):
+    """Batched first-order certificate (diagnostics.hpp:22-55); 0 certifies optimality."""
+    torch = _torch()
+    box = box or BoxConstraint.unconstrained()
+    host = not _is_cuda(points)
+    P = _dev(points)
+    if P.dim() == 2:
+        P = P.unsqueeze(0)
+    B, n, d = P.shape
+    Wt = _dev(weights, device=P.device).reshape(B, n)
+    Z = _dev(z, device=P.device).reshape(B, d)
+    out = torch.empty(B, device=P.device)
+    f = L.Failure()
+    with torch.cuda.device(P.device):
+        st = L.load().nlem_optimality_residual_batched(_ptr(P), _ptr(Wt), B, n, d, box.c(), _ptr(Z),
+                                                       _ptr(out), C.byref(f), _stream(P.device))
+    _raise(st, f)
+    return _out(host, out)

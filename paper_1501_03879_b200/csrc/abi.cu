@@ -254,6 +254,52 @@ int64_t mirror_host(int64_t i, int64_t n) {
 
 extern "C" {
 
+nlem_status nlem_frames_psnr(const float* frames, const float* clean, int64_t nframes,
+                             int64_t count, double* psnr_out, nlem_failure* failure, void* stream) {
+  clear(failure);
+  if (nframes < 0 || count < 1) return invalid(failure, "psnr needs non-empty frames");
+  if (nframes == 0) return NLEM_OK;
+  if (!frames || !clean || !psnr_out) return invalid(failure, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* sse = nullptr;
+  cudaError_t e = cudaMallocAsync(&sse, sizeof(double) * nframes, s);
+  if (e == cudaSuccess) e = launch_frames_sse(frames, clean, nframes, count, sse, s);
+  std::vector<double> h(static_cast<size_t>(nframes));
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), sse, sizeof(double) * nframes, cudaMemcpyDeviceToHost, s);
+  if (sse) cudaFreeAsync(sse, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  for (int64_t t = 0; t < nframes; ++t) {  // psnr.hpp:20-24
+    const double mse = h[t] / static_cast<double>(count);
+    psnr_out[t] = mse == 0.0 ? HUGE_VAL : 10.0 * std::log10(255.0 * 255.0 / mse);
+  }
+  return NLEM_OK;
+}
+
+nlem_status nlem_optimality_residual_batched(const float* points, const float* weights,
+                                             int64_t batch, int64_t n, int64_t d, nlem_box box,
+                                             const float* z, float* residual_out,
+                                             nlem_failure* failure, void* stream) {
+  clear(failure);
+  if (batch < 0) return invalid(failure, "batch must be nonnegative");
+  if (n < 1) return invalid(failure, "point set must contain at least one point");
+  if (d < 1 || d > kMaxDim) return invalid(failure, "point dimension must be in [1, 1024]");
+  if (nlem_status st = check_box(box, failure)) return st;
+  if (batch == 0) return NLEM_OK;
+  if (!points || !weights || !z || !residual_out) return invalid(failure, "null buffer");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (failure) {
+    if (nlem_status st = validate_points_dev(points, weights, batch, static_cast<int>(n),
+                                             static_cast<int>(d), failure, s))
+      return st;
+  }
+  cudaError_t e = launch_optimality(points, weights, z, batch, static_cast<int>(n),
+                                    static_cast<int>(d), box, residual_out, s);
+  if (e == cudaSuccess && failure) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(failure, e);
+  return NLEM_OK;
+}
+
 const char* nlem_version(void) { return "nlem_b200 0.1 (sm_100a)"; }
 
 const char* nlem_status_string(nlem_status s) {

@@ -1,0 +1,170 @@
+// Auxiliary device reductions next to the hot path:
+//  * per-frame squared error -> PSNR for snapshot sweeps (proj/include/nlem/psnr.hpp:12-24),
+//    so convergence curves need no T x H x W device-to-host copy;
+//  * batched first-order optimality certificate (proj/include/nlem/diagnostics.hpp:22-55),
+//    certifying batched EM-ADMM outputs at scale without the CPU oracle.
+// Both reductions use fixed orders (deterministic).
+#include <algorithm>
+
+#include "launch.h"
+
+namespace nlemk {
+
+constexpr int kPsnrThreads = 256;
+
+// partial SSE (double) of frame f over block chunk b -> part[f * nblk + b]
+__global__ void __launch_bounds__(kPsnrThreads)
+frame_sse_kernel(const float* __restrict__ frames, const float* __restrict__ clean, int64_t count,
+                 int nblk, double* part) {
+  const int f = blockIdx.y, b = blockIdx.x;
+  const float* fr = frames + static_cast<int64_t>(f) * count;
+  const int64_t chunk = (count + nblk - 1) / nblk;
+  const int64_t i0 = b * chunk, i1 = i0 + chunk < count ? i0 + chunk : count;
+  double acc = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += kPsnrThreads) {
+    const double d = static_cast<double>(fr[i]) - static_cast<double>(clean[i]);
+    acc = fma(d, d, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double w[kPsnrThreads / 32];
+  if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kPsnrThreads / 32; ++i) t += w[i];
+    part[static_cast<int64_t>(f) * nblk + b] = t;
+  }
+}
+
+__global__ void frame_sse_finish(const double* part, int nblk, int nframes, double* sse) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= nframes) return;
+  double t = 0.0;
+  for (int b = 0; b < nblk; ++b) t += part[static_cast<int64_t>(f) * nblk + b];
+  sse[f] = t;
+}
+
+cudaError_t launch_frames_sse(const float* frames, const float* clean, int64_t nframes,
+                              int64_t count, double* sse_dev, cudaStream_t stream) {
+  const int nblk = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(2 * device_caps().sms, (count + kPsnrThreads - 1) / kPsnrThreads)));
+  double* part = nullptr;
+  cudaError_t e = cudaMallocAsync(&part, sizeof(double) * nblk * nframes, stream);
+  if (e != cudaSuccess) return e;
+  frame_sse_kernel<<<dim3(nblk, static_cast<unsigned>(nframes)), kPsnrThreads, 0, stream>>>(
+      frames, clean, count, nblk, part);
+  frame_sse_finish<<<static_cast<unsigned>((nframes + 127) / 128), 128, 0, stream>>>(
+      part, nblk, static_cast<int>(nframes), sse_dev);
+  e = cudaGetLastError();
+  cudaFreeAsync(part, stream);
+  return e;
+}
+
+// One CTA (256 threads, warp per point) per problem: diagnostics.hpp:22-55 in float with the
+// reference's 1e-12 coincidence threshold and active-face absorption.
+template <int JPL>
+__global__ void __launch_bounds__(256)
+optimality_kernel(const float* __restrict__ points, const float* __restrict__ weights,
+                  const float* __restrict__ z, int64_t batch, int n, int d, nlem_box box,
+                  float* out) {
+  extern __shared__ float sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int W = 8;
+  float* gpart = sm;             // [W][d]
+  float* ball = sm + W * d;      // [W]
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const float* a = points + b * static_cast<int64_t>(n) * d;
+    const float* zb = z + b * d;
+    float zv[JPL], g[JPL];
+#pragma unroll
+    for (int q = 0; q < JPL; ++q) {
+      const int j = lane + 32 * q;
+      zv[q] = j < d ? zb[j] : 0.0f;
+      g[q] = 0.0f;
+    }
+    float bl = 0.0f;
+    for (int k = warp; k < n; k += W) {
+      const float* ak = a + static_cast<int64_t>(k) * d;
+      float diff[JPL];
+      float s2 = 0.0f;
+#pragma unroll
+      for (int q = 0; q < JPL; ++q) {
+        const int j = lane + 32 * q;
+        diff[q] = j < d ? zv[q] - ak[j] : 0.0f;
+        s2 = fmaf(diff[q], diff[q], s2);
+      }
+      s2 = warp_sum(s2);
+      const float dist = sqrtf(s2);
+      const float w = weights[b * n + k];
+      if (dist <= 1e-12f) {
+        bl += w;
+      } else {
+        const float f = w / dist;
+#pragma unroll
+        for (int q = 0; q < JPL; ++q) g[q] = fmaf(f, diff[q], g[q]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < JPL; ++q) {
+      const int j = lane + 32 * q;
+      if (j < d) gpart[warp * d + j] = g[q];
+    }
+    if (lane == 0) ball[warp] = bl;
+    __syncthreads();
+    if (warp == 0) {
+      float n2 = 0.0f;
+      bool inbox = true;
+      for (int j = lane; j < d; j += 32) {
+        if (box.bounded) inbox &= zb[j] >= box.lower && zb[j] <= box.upper;
+        float gj = 0.0f;
+        for (int w = 0; w < W; ++w) gj += gpart[w * d + j];
+        if (box.bounded) {
+          const bool lo = zb[j] == box.lower, hi = zb[j] == box.upper;
+          if (lo && hi) gj = 0.0f;
+          else if (hi) gj = fmaxf(gj, 0.0f);  // the face absorbs any push upward
+          else if (lo) gj = fminf(gj, 0.0f);
+        }
+        n2 = fmaf(gj, gj, n2);
+      }
+      n2 = warp_sum(n2);
+      if (lane == 0) {
+        float bt = 0.0f;
+        for (int w = 0; w < W; ++w) bt += ball[w];
+        out[b] = fmaxf(0.0f, sqrtf(n2) - bt);
+      }
+      if (!__all_sync(0xffffffffu, inbox) && lane == 0) {
+        out[b] = __int_as_float(0x7fc00000);  // z outside the box: the reference throws
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_optimality(const float* points, const float* weights, const float* z,
+                              int64_t batch, int n, int d, nlem_box box, float* out,
+                              cudaStream_t stream) {
+  const size_t smem = (8 * static_cast<size_t>(d) + 8) * sizeof(float);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batch, device_caps().sms * 8));
+  const int jpl = d <= 32 ? 1 : d <= 64 ? 2 : d <= 128 ? 4 : d <= 256 ? 8 : d <= 512 ? 16 : 32;
+  switch (jpl) {
+#define NLEM_OPT_CASE(J)                                                                          \
+  case J:                                                                                         \
+    cudaFuncSetAttribute(optimality_kernel<J>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                         static_cast<int>(smem));                                                 \
+    optimality_kernel<J><<<static_cast<unsigned>(grid), 256, smem, stream>>>(points, weights, z,  \
+                                                                             batch, n, d, box,    \
+                                                                             out);                \
+    break;
+    NLEM_OPT_CASE(1)
+    NLEM_OPT_CASE(2)
+    NLEM_OPT_CASE(4)
+    NLEM_OPT_CASE(8)
+    NLEM_OPT_CASE(16)
+    NLEM_OPT_CASE(32)
+#undef NLEM_OPT_CASE
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nlemk

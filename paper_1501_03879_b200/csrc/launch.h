@@ -93,6 +93,12 @@ cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_fast_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_fast(const NlemLaunch& L, cudaStream_t stream);
 
+cudaError_t launch_frames_sse(const float* frames, const float* clean, int64_t nframes,
+                              int64_t count, double* sse_dev, cudaStream_t stream);
+cudaError_t launch_optimality(const float* points, const float* weights, const float* z,
+                              int64_t batch, int n, int d, nlem_box box, float* out,
+                              cudaStream_t stream);
+
 // validation kernels (types.hpp:58-68, image.hpp:14-17): packed (index << 2 | code), ~0 = ok
 cudaError_t launch_validate_points(const float* points, const float* weights, int64_t batch,
                                    int n, int d, unsigned long long* result, cudaStream_t stream);

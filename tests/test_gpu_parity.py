@@ -295,3 +295,41 @@ def test_host_entry_matches_device(nb):
     clean, noisy = synth.noisy_image(64, 64, 8, 5, 20.0)
     p = nb.NlemParams(search=11, patch=5, h=synth.reference_h(20.0, 25), solver_iters=5, mu=1.0)
     assert (nb.nlem_denoise_host(noisy, p) == nb.nlem_denoise(noisy, p)).all()
+
+
+# ---------------------------------------------------------------- §8f next rows
+def test_frames_psnr_matches_oracle(nb, oracle):
+    """Device PSNR per snapshot frame (psnr.hpp:12-24) == the oracle's on the same frames."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(64, 48, 8, 5, 25.0)
+    p = nb.NlemParams(search=21, patch=7, h=synth.reference_h(25.0, 49), solver_iters=8, mu=1.0,
+                      init_mode="nlm")
+    frames = nb.nlem_denoise_snapshots(noisy, p)
+    got = nb.frames_psnr(frames, clean)
+    ref = np.array([oracle.psnr(clean.astype(np.float64), frames[t].astype(np.float64))
+                    for t in range(frames.shape[0])])
+    np.testing.assert_allclose(got, ref, rtol=1e-10)
+    assert np.isinf(nb.frames_psnr(np.stack([clean, clean]), clean)).all()  # identical -> +inf
+
+
+def test_optimality_certificate(nb, oracle):
+    """Batched diagnostics.hpp:22-55: converged ADMM outputs certify (test_diagnostics.cpp:72-90),
+    and the GPU residual matches the oracle's on the same z."""
+    rng = np.random.default_rng(72)
+    B, n, d = 8, 15, 3
+    pts = rng.uniform(0, 1, size=(B, n, d)).astype(np.float32)
+    w = rng.uniform(0.5, 1.5, size=(B, n)).astype(np.float32)
+    for box in (None, (0.4, 0.6)):
+        nbox = nb.BoxConstraint.interval(*box) if box else nb.BoxConstraint.unconstrained()
+        r = nb.admm_euclidean_median(pts, w, nbox, nb.AdmmConfig(mu=2.0, max_iter=4000, tol_primal=-1.0))
+        res = nb.optimality_residual(pts, w, r.minimizer, nbox)
+        for b in range(B):
+            fbox = None if box is None else (float(np.float32(box[0])), float(np.float32(box[1])))
+            ref = oracle.optimality_residual(pts[b].astype(np.float64), w[b].astype(np.float64),
+                                             r.minimizer[b].astype(np.float64), fbox)
+            assert abs(res[b] - ref) <= 1e-4 * w[b].sum()
+        assert (res <= 1e-3 * w.sum(1)).all()  # acceptance_main.cpp:221-244 bar
+    # a non-optimal point has a clearly positive residual
+    bad = nb.optimality_residual(pts, w, np.full((B, d), 0.9, np.float32))
+    assert (bad > 1e-2).all()
