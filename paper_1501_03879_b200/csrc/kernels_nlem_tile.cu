@@ -23,6 +23,12 @@ namespace nlemk {
 // Debug-only: clock64 stamps of sweep phases for the first pixels of CTA 0 (warp 0, lane 0
 // and the last warp's lane 0), read back by nlem_debug_phase_times.
 __device__ long long g_phase[2][64][16];
+__device__ long long g_warp[32][64][4];  // per warp lane 0: sweep start, red written, after B1, after B2
+#define WSTAMP(slot)                                                                        \
+  do {                                                                                     \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && X.dbg_it < 64)                        \
+      g_warp[threadIdx.x >> 5][X.dbg_it][slot] = clock64();                                 \
+  } while (0)
 #define PHASE(slot)                                                                            \
   do {                                                                                        \
     if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32) && X.dbg_it < 64) \
@@ -31,6 +37,9 @@ __device__ long long g_phase[2][64][16];
 #else
 #define PHASE(slot) \
   do {              \
+  } while (0)
+#define WSTAMP(slot) \
+  do {               \
   } while (0)
 #endif
 
@@ -270,7 +279,9 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
 #pragma unroll
     for (int dc = 0; dc < C::KS; ++dc) row[dc] = v[dc];
   }
+  WSTAMP(1);
   __syncthreads();
+  WSTAMP(2);
   PHASE(6);
   const int j = X.tid / C::CPT, part = X.tid % C::CPT;
   float s = 0.0f;
@@ -320,6 +331,7 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
   if (j < C::D && part == 0) finish(j, s);
   PHASE(9);
   __syncthreads();
+  WSTAMP(3);
   PHASE(10);
 }
 
@@ -746,6 +758,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         __syncthreads();
         for (int t = 1; t <= P.iters; ++t) {
           PHASE(0);
+          WSTAMP(0);
           // (U) p' = s p + (c - a); per-point norm partials
           float nr[C::KB];
           {
@@ -905,6 +918,9 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
 }  // namespace nlemk
 extern "C" int nlem_debug_phase_times(long long* out /* [2][64][16] */) {
   return cudaMemcpyFromSymbol(out, nlemk::g_phase, sizeof(nlemk::g_phase)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int nlem_debug_warp_times(long long* out /* [32][64][4] */) {
+  return cudaMemcpyFromSymbol(out, nlemk::g_warp, sizeof(nlemk::g_warp)) == cudaSuccess ? 0 : 1;
 }
 namespace nlemk {
 #endif

@@ -45,3 +45,20 @@ for w in range(2):
     for k, n in enumerate(names):
         print(f"   {n:28s} mean {a[:, k].mean():8.1f}  median {np.median(a[:, k]):8.1f}")
     print(f"   total per sweep (median)     {np.median(a[:, :5].sum(1) + a[:, 5]):8.1f}")
+
+wb = np.zeros((32, 64, 4), np.int64)
+assert lib.nlem_debug_warp_times(wb.ctypes.data_as(C.POINTER(C.c_longlong))) == 0
+nw = 16
+rows = []
+for it in range(4, 60):
+    st = wb[:nw, it, 0]
+    if (st == 0).any() or (wb[:nw, it + 1, 0] == 0).any():
+        continue
+    t0 = st.min()
+    rows.append([st - t0, wb[:nw, it, 1] - t0, wb[:nw, it, 2] - t0, wb[:nw, it, 3] - t0,
+                 wb[:nw, it + 1, 0] - t0])
+a = np.array(rows)  # [sweeps, 5, warps]
+med = np.median(a, axis=0)
+print("per-warp median cycles since the earliest sweep start (sweep start, red written, after B1, after B2, next start):")
+for w in range(nw):
+    print(f"  warp {w:2d}: " + "  ".join(f"{x:7.0f}" for x in med[:, w]))
