@@ -64,11 +64,15 @@ def load(build_if_missing: bool = True):
     global _lib
     if _lib is not None:
         return _lib
-    if build_if_missing:
+    so_path = SO_PATH
+    variant = os.environ.get("NLEM_LIB_VARIANT", "")  # A/B builds (build.py --variant=...)
+    if variant:
+        so_path = _build.variant_path(variant)
+    elif build_if_missing:
         _build.build()
-    if not os.path.exists(SO_PATH):
-        raise RuntimeError(f"NLEM CUDA library missing: {SO_PATH} (run paper_1501_03879_b200.build)")
-    L = C.CDLL(SO_PATH)
+    if not os.path.exists(so_path):
+        raise RuntimeError(f"NLEM CUDA library missing: {so_path} (run paper_1501_03879_b200.build)")
+    L = C.CDLL(so_path)
     vp = C.c_void_p
     L.nlem_version.restype = C.c_char_p
     L.nlem_status_string.restype = C.c_char_p

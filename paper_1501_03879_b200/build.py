@@ -39,26 +39,42 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+# experimental build variants (A/B and debug only): "_"-separated tokens -> defines
+_VARIANT_TOKENS = {
+    "prof": "-DNLEM_PHASE_PROFILE",  # clock64 phase stamps (nlem_debug_phase_times)
+    "cl2": "-DNLEM_TILE_CL=2",       # 2-CTA cluster tile kernel
+    "xw0": "-DNLEM_TILE_XW=0",       # consensus spread over the point warps
+    "xw1": "-DNLEM_TILE_XW=1",       # dedicated consensus warp
+}
+
+
+def variant_path(variant: str) -> str:
+    return SO if not variant else SO.replace(".so", f"_{variant}.so")
+
+
 def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
-    """variant="prof": debug build with NLEM_PHASE_PROFILE into _lib/libnlem_b200_prof.so."""
-    so = SO if not variant else SO.replace(".so", f"_{variant}.so")
+    """variant="prof" etc.: debug / A-B builds into _lib/libnlem_b200_<variant>.so."""
+    so = variant_path(variant)
     if not force and not variant and not _stale():
         return SO
     os.makedirs(OUT_DIR, exist_ok=True)
-    objs = []
+    extra = [_VARIANT_TOKENS[t] for t in variant.split("_") if t]
+    tag = f"_{variant}" if variant else ""
+    jobs = []
     for src in sources():
-        obj = os.path.join(OUT_DIR, os.path.basename(src) + ".o")
+        obj = os.path.join(OUT_DIR, os.path.basename(src) + tag + ".o")
         if src.endswith(".cu"):
-            extra = ["-DNLEM_PHASE_PROFILE"] if variant.startswith("prof") else []
-            if variant == "prof_cl2":
-                extra.append("-DNLEM_TILE_CL=2")
             cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++20", "-fPIC", "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
+        jobs.append((cmd, obj))
+    procs = [subprocess.Popen(cmd) for cmd, _ in jobs]  # one nvcc per translation unit
+    failed = [cmd for (cmd, _), p in zip(jobs, procs) if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
+    objs = [obj for _, obj in jobs]
     tmp = so + ".tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-lpthread"]
@@ -70,5 +86,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True,
-                variant="prof" if "--prof" in sys.argv else ""))
+    var = next((a.split("=", 1)[1] for a in sys.argv if a.startswith("--variant=")), "")
+    if "--prof" in sys.argv:
+        var = "prof"
+    print(build(force="--force" in sys.argv, verbose=True, variant=var))

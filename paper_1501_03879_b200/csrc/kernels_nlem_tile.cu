@@ -43,7 +43,7 @@ __device__ long long g_warp[32][64][4];  // per warp lane 0: sweep start, red wr
   } while (0)
 #endif
 
-template <int KS_, int SW_, int KB_, int CL_>
+template <int KS_, int SW_, int KB_, int CL_, int XW_ = 0>
 struct TileCfg {
   static constexpr int KS = KS_;                 // patch side k
   static constexpr int SW = SW_;                 // search window side S
@@ -55,8 +55,9 @@ struct TileCfg {
   static constexpr int NGROUPS = SW * NBLK;
   static constexpr int CL = CL_;                 // CTAs per pixel (thread-block cluster)
   static constexpr int NGC = (NGROUPS + CL - 1) / CL;  // groups per CTA
-  static constexpr int WARPS = (NGC + GPW - 1) / GPW;
-  static constexpr int THREADS = 32 * WARPS;
+  static constexpr int WARPS = (NGC + GPW - 1) / GPW;  // point warps
+  static constexpr int XW = XW_;                 // + a dedicated consensus warp (CL == 1)
+  static constexpr int THREADS = 32 * (WARPS + XW);
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
   static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
@@ -65,15 +66,22 @@ struct TileCfg {
   static constexpr int NE = ((KP - 1 + (KS - 1) / 2) > ((SEG - 1) / 2) ? (KP - 1 + (KS - 1) / 2)
                                                                         : ((SEG - 1) / 2)) + 1;
   static constexpr int NO = KP - 1 + (KS - 2) / 2 + 1;
-  static constexpr int KBP = (KB + 3) & ~3;      // padded per-lane norm row
+  // per-lane norm row of the group transpose.  k = 7: 31 = the smallest stride >= KB for which
+  // both the row writes (fixed m, 28 lanes) and the column reads (fixed r) are bank-conflict
+  // free (a stride of 8 made every write 7-way conflicted); k = 5 has no conflict-free stride
+  static constexpr int KBP = (KS == 7 && KB == 7) ? 31 : (KB + 3) & ~3;
   static constexpr int KSP = KS;                 // per-lane coordinate row (unpadded)
   // per-group block of g partials: D floats padded so that CPT consecutive-part blocks land
   // on disjoint bank quads (part * GSTR mod 32 in steps of 4): 52 for D = 49, CPT = 8
-  static constexpr int GSTR = D == 49 ? 52 : ((D + 3) & ~3) + (((((D + 3) & ~3) / 4) % 2) ? 0 : 4);
+  // (with a consensus warp, D = 49: 56 = the smallest even stride >= D + 2 whose row writes
+  // are conflict-free; the consensus warp's float2 row reads are conflict-free for any stride)
+  static constexpr int GSTR = (XW_ && D == 49) ? 56
+                              : D == 49 ? 52 : ((D + 3) & ~3) + (((((D + 3) & ~3) / 4) % 2) ? 0 : 4);
   static constexpr int SPL = (KB + G - 1) / G;   // points whose prox scale a lane computes
   static constexpr int CPT = THREADS >= 8 * D ? 8 : THREADS >= 4 * D ? 4 : THREADS >= 2 * D ? 2 : 1;
   static_assert(SW % KB == 0, "segments tile the grid row");
   static_assert(D <= THREADS, "consensus needs one thread per coordinate");
+  static_assert(XW == 0 || (CL == 1 && D <= 64), "consensus warp: one CTA, <= 2 coordinates per lane");
 };
 
 // configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
@@ -84,15 +92,19 @@ struct TileCfg {
 // 1: one CTA per pixel (16 warps) — production.  2: pixel split over a 2-CTA cluster with a
 // DSMEM + mbarrier exchange per sweep — experimental: measured slower, the per-sweep exchange
 // waits ~1.2-1.7k cycles on skew between the two SMs (profiles/r1_tile_phase_times.txt)
-using TileK7S21 = TileCfg<7, 21, 7, NLEM_TILE_CL>;
+// dedicated consensus warp (1, production) or consensus spread over the point warps (0)
+#ifndef NLEM_TILE_XW
+#define NLEM_TILE_XW 0
+#endif
+using TileK7S21 = TileCfg<7, 21, 7, NLEM_TILE_CL, NLEM_TILE_CL == 1 ? NLEM_TILE_XW : 0>;
 using TileK5S11 = TileCfg<5, 11, 11, 1>;   // config 0: 11 groups of 5 lanes, 2 warps
 
 template <class C>
 struct TileSmem {
   static constexpr int T = C::TH * C::TWS;            // one tile copy
   static constexpr int ROWS = C::NGC * C::G + 40;  // local groups + dummy rows for idle lanes
-  static constexpr int NB = ROWS * C::KBP;               // norm transpose
-  static constexpr int RED = (C::NGC + 8) * C::GSTR;     // g partials (+ dummy groups)
+  static constexpr int NB = (ROWS * C::KBP + 3) & ~3;    // norm transpose (16-byte multiple)
+  static constexpr int RED = ((C::NGC + 8) * C::GSTR + 3) & ~3;  // g partials (+ dummy groups)
   static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
                                C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
                                4 /*mbarrier*/;
@@ -146,6 +158,13 @@ __device__ __forceinline__ float2 tsub2(float2 a, float2 b) {
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
 __device__ __forceinline__ float2 tfma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+// named CTA barriers (id 0 is __syncthreads): producers arrive without waiting
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 // Per-lane register image of its tile segment t[0..SEG): E[i] = (t[2i], t[2i+1]),
 // O[i] = (t[2i+1], t[2i+2]).  a_{m,dc} = t[m+dc].
@@ -736,7 +755,179 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           __syncthreads();
         }
       }
-      if (P.solver == NLEM_SOLVER_ADMM) {
+      if constexpr (C::XW == 1) {
+        if (P.solver == NLEM_SOLVER_ADMM) {
+          // ---- EM-ADMM sweeps, split p-form with a dedicated consensus warp.  Between sweeps
+          // a lane keeps q_k = s_k p_k - a_k; sweep t forms p_k = q_k + c (c = 2 z_{t-1} - z_{t-2}),
+          // the norms, prox scales and g partials (the critical path), hands the partials in
+          // with a non-blocking barrier arrive, and computes the next q while the consensus
+          // warp reduces the partials and publishes z_t and c.  Same iterates as the p-form
+          // (p' = s p + (c - a)) up to FP32 rounding order.
+          if (X.tid < C::D) X.c2[X.tid] = tf2(X.z[X.tid]);
+          __syncthreads();
+          if (X.warp < C::WARPS) {
+            float lam_own[C::SPL];
+#pragma unroll
+            for (int i = 0; i < C::SPL; ++i) lam_own[i] = inv_mu * wown[i];
+            float2 p2[C::KP][C::KS];  // q between sweeps, p within a sweep
+            float p1[C::KS];
+#pragma unroll
+            for (int qq = 0; qq < C::KP; ++qq)
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) p2[qq][dc] = tsub2(make_float2(0.0f, 0.0f), S.pair(qq, dc));
+#pragma unroll
+            for (int dc = 0; dc < C::KS; ++dc) p1[dc] = C::ODD ? -S.single(dc) : 0.0f;
+            float* red_row = X.red + (X.grow0 / C::G) * C::GSTR + X.dr * C::KS;
+            for (int t = 1; t <= P.iters; ++t) {
+              WSTAMP(0);
+              float nr[C::KB];
+              {
+                float2 cc[C::KS];
+#pragma unroll
+                for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
+#pragma unroll
+                for (int qq = 0; qq < C::KP; ++qq) {
+                  float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                  for (int dc = 0; dc < C::KS; ++dc) {
+                    p2[qq][dc] = __fadd2_rn(p2[qq][dc], cc[dc]);
+                    acc = tfma2(p2[qq][dc], p2[qq][dc], acc);
+                  }
+                  nr[2 * qq] = acc.x;
+                  nr[2 * qq + 1] = acc.y;
+                }
+                if (C::ODD) {
+                  float acc = 0.0f;
+#pragma unroll
+                  for (int dc = 0; dc < C::KS; ++dc) {
+                    p1[dc] += cc[dc].x;
+                    acc = fmaf(p1[dc], p1[dc], acc);
+                  }
+                  nr[C::KB - 1] = acc;
+                }
+              }
+              float tot[C::SPL], sown[C::SPL];
+              group_point_totals<C>(X, nr, tot);
+              int fbits = 0;
+#pragma unroll
+              for (int i = 0; i < C::SPL; ++i) {
+                const float lam = lam_own[i];
+                const float s = lam != 0.0f ? fminf(1.0f, lam * rsqrt_ftz(tot[i])) : 0.0f;
+                sown[i] = s;
+                fbits |= (lam != 0.0f && !isfinite(tot[i])) ? 1 : 0;
+                if (static_eq) fbits |= (is_real(X.dr + i * C::G) && s != 1.0f) ? 2 : 0;
+              }
+              float sall[C::KB];
+              group_broadcast<C>(X, sown, sall);
+              float2 s2[C::KP];
+#pragma unroll
+              for (int qq = 0; qq < C::KP; ++qq) s2[qq] = make_float2(sall[2 * qq], sall[2 * qq + 1]);
+              const float s1 = C::ODD ? sall[C::KB - 1] : 0.0f;
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) {
+                float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+                for (int qq = 0; qq < C::KP; ++qq) acc = tfma2(s2[qq], p2[qq][dc], acc);
+                float tsum = acc.x + acc.y;
+                if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
+                red_row[dc] = X.active ? tsum : 0.0f;
+              }
+              fbits = __reduce_or_sync(0xffffffffu, fbits);
+              if (X.lane == 0 && fbits) atomicOr(&X.flags[t & 1], fbits);
+              WSTAMP(1);
+              named_bar_arrive(1, C::THREADS);
+              // next sweep's q = s p - a, overlapping the consensus
+#pragma unroll
+              for (int qq = 0; qq < C::KP; ++qq)
+#pragma unroll
+                for (int dc = 0; dc < C::KS; ++dc) {
+                  const float2 a = S.pair(qq, dc);
+                  p2[qq][dc] = tfma2(s2[qq], p2[qq][dc], make_float2(-a.x, -a.y));
+                }
+              if (C::ODD) {
+#pragma unroll
+                for (int dc = 0; dc < C::KS; ++dc) p1[dc] = fmaf(s1, p1[dc], -S.single(dc));
+              }
+              WSTAMP(2);
+              named_bar_sync(2, C::THREADS);
+              WSTAMP(3);
+              const int fl = X.flags[t & 1];
+#ifdef NLEM_PHASE_PROFILE
+              ++X.dbg_it;
+#endif
+              if (fl & (4 | 1)) {
+                fail_iter = (fl & 4) || t == 1 ? t : t - 1;
+                fail_kind = NLEM_FAIL_ADMM_ITERATE;
+                break;
+              }
+              if (frames && X.tid == 0)
+                frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
+              if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
+                iters = t;
+                break;
+              }
+            }
+          } else {
+            // consensus warp: lane l owns coordinates 2l, 2l+1; fixed-order sum over the groups
+            // (8 interleaved chains, then a tree), z_t = P_C(z - g/n), c = 2 z_t - z
+            const int j = 2 * X.lane;
+            const bool own = j < C::D;
+            const float2* col = reinterpret_cast<const float2*>(X.red + (own ? j : 0));
+            static_assert(C::GSTR % 2 == 0 && C::GSTR >= C::D + 1, "float2 coordinate pairs");
+            for (int t = 1; t <= P.iters; ++t) {
+              WSTAMP(0);
+              named_bar_sync(1, C::THREADS);
+              WSTAMP(1);
+              float2 ch[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) ch[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+              for (int g = 0; g < C::NGC; ++g) {
+                const float2 v = col[g * (C::GSTR / 2)];
+                ch[g % 8].x += v.x;
+                ch[g % 8].y += v.y;
+              }
+#pragma unroll
+              for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+                for (int i = 0; i + w < 8; i += 2 * w) {
+                  ch[i].x += ch[i + w].x;
+                  ch[i].y += ch[i + w].y;
+                }
+              int f = 0;
+              if (own) {
+                const float gs[2] = {ch[0].x, ch[0].y};
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                  const int jj = j + e;
+                  if (jj < C::D) {
+                    const float zo = X.z[jj];
+                    const float zn = clamp_box(fmaf(-gs[e], inv_n, zo), P.range);
+                    f |= isfinite(zn) ? 0 : 4;
+                    if (static_eq) f |= (zn != X.a0[jj]) ? 8 : 0;
+                    X.z[jj] = zn;
+                    X.c2[jj] = tf2(2.0f * zn - zo);
+                  }
+                }
+              }
+              f = __reduce_or_sync(0xffffffffu, f);
+              if (X.lane == 0) {
+                if (f) atomicOr(&X.flags[t & 1], f);
+                X.flags[(t + 1) & 1] = 0;  // every read of sweep t-1's word is done
+              }
+              __syncwarp();
+              const int fl = X.flags[t & 1];
+              WSTAMP(2);
+              named_bar_arrive(2, C::THREADS);
+#ifdef NLEM_PHASE_PROFILE
+              ++X.dbg_it;
+#endif
+              if (fl & (4 | 1)) break;
+              if (static_eq && !(fl & 2) && !(fl & 8)) break;
+            }
+          }
+        }
+      } else if (P.solver == NLEM_SOLVER_ADMM) {
         // ---- EM-ADMM sweeps in p-form (see solver_generic.cuh)
         float lam_own[C::SPL];
 #pragma unroll
