@@ -45,6 +45,9 @@ _VARIANT_TOKENS = {
     "cl2": "-DNLEM_TILE_CL=2",       # 2-CTA cluster tile kernel
     "xw0": "-DNLEM_TILE_XW=0",       # consensus spread over the point warps
     "xw1": "-DNLEM_TILE_XW=1",       # dedicated consensus warp
+    "xw2": "-DNLEM_TILE_XW=2",       # last-arriving warp runs the consensus
+    "xw3": "-DNLEM_TILE_XW=3",       # warp pre-reduction + one consensus warp
+    "xw4": "-DNLEM_TILE_XW=4",       # warp pre-reduction + CPT consensus, split p-form
 }
 
 

@@ -56,8 +56,15 @@ struct TileCfg {
   static constexpr int CL = CL_;                 // CTAs per pixel (thread-block cluster)
   static constexpr int NGC = (NGROUPS + CL - 1) / CL;  // groups per CTA
   static constexpr int WARPS = (NGC + GPW - 1) / GPW;  // point warps
-  static constexpr int XW = XW_;                 // + a dedicated consensus warp (CL == 1)
-  static constexpr int THREADS = 32 * (WARPS + XW);
+  // consensus mode (CL == 1 only for 1, 2): 0 = CPT threads per coordinate over all warps
+  // between two CTA barriers; 1 = a dedicated extra consensus warp; 2 = the last point warp
+  // to hand in its partials (smem arrival counter) runs the consensus; 3 = each warp pre-reduces
+  // its groups' partials into one warp row, one CTA barrier, then the last warp alone runs the
+  // consensus over the warp rows while the others prepare the next sweep's state; 4 = warp
+  // pre-reduction, then CPT threads per coordinate over the warp rows (all warps), with the
+  // next sweep's state update issued between the consensus loads and their reduction
+  static constexpr int XW = XW_;
+  static constexpr int THREADS = 32 * (WARPS + (XW == 1 ? 1 : 0));
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
   static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
@@ -82,6 +89,8 @@ struct TileCfg {
   static_assert(SW % KB == 0, "segments tile the grid row");
   static_assert(D <= THREADS, "consensus needs one thread per coordinate");
   static_assert(XW == 0 || (CL == 1 && D <= 64), "consensus warp: one CTA, <= 2 coordinates per lane");
+  static_assert(XW != 2 || NGC <= 64, "arrival-counter consensus: 8 chains x 8 rows");
+  static_assert(XW != 4 || WARPS % CPT == 0, "warp rows split evenly over the CPT parts");
 };
 
 // configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
@@ -94,7 +103,7 @@ struct TileCfg {
 // waits ~1.2-1.7k cycles on skew between the two SMs (profiles/r1_tile_phase_times.txt)
 // dedicated consensus warp (1, production) or consensus spread over the point warps (0)
 #ifndef NLEM_TILE_XW
-#define NLEM_TILE_XW 0
+#define NLEM_TILE_XW 4
 #endif
 using TileK7S21 = TileCfg<7, 21, 7, NLEM_TILE_CL, NLEM_TILE_CL == 1 ? NLEM_TILE_XW : 0>;
 using TileK5S11 = TileCfg<5, 11, 11, 1>;   // config 0: 11 groups of 5 lanes, 2 warps
@@ -104,7 +113,8 @@ struct TileSmem {
   static constexpr int T = C::TH * C::TWS;            // one tile copy
   static constexpr int ROWS = C::NGC * C::G + 40;  // local groups + dummy rows for idle lanes
   static constexpr int NB = (ROWS * C::KBP + 3) & ~3;    // norm transpose (16-byte multiple)
-  static constexpr int RED = ((C::NGC + 8) * C::GSTR + 3) & ~3;  // g partials (+ dummy groups)
+  static constexpr int RED = ((C::NGC + 8 + C::WARPS) * C::GSTR + 3) & ~3;  // g partials per group
+                                                   // (+ dummy groups) and per warp (XW >= 3)
   static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
                                C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
                                4 /*mbarrier*/;
@@ -189,6 +199,7 @@ struct TileCtx {
   float* T1;    // tile shifted left by one column
   float* nbuf;  // [NGROUPS][G][KBP]
   float* red;   // [NGC + 8][GSTR] per-group g partials
+  float* wred;  // [WARPS][GSTR] per-warp g partials (XW >= 3)
   float2* c2;   // [D]
   float* z;     // [D]
   float* a0;    // [D]
@@ -210,6 +221,7 @@ struct TileCtx {
     T1 = T0 + TileSmem<C>::T;
     nbuf = T1 + TileSmem<C>::T;
     red = nbuf + TileSmem<C>::NB;
+    wred = red + (C::NGC + 8) * C::GSTR;
     c2 = reinterpret_cast<float2*>(red + TileSmem<C>::RED);
     z = reinterpret_cast<float*>(c2 + C::D);
     a0 = z + C::D;
@@ -230,7 +242,9 @@ struct TileCtx {
     q = rank * C::NGC + lq;             // global group
     nloc = min(C::NGC, C::NGROUPS - rank * C::NGC);
     active = ql < C::GPW && lq < nloc;
-    grow0 = active ? lq * C::G : C::NGC * C::G + base;  // idle lanes: private dummy rows
+    // lanes of a group slot without a real group keep their slot's rows (all-zero partials, so
+    // per-warp sums over GPW rows stay exact); lanes outside any slot get private dummy rows
+    grow0 = ql < C::GPW ? lq * C::G : C::NGC * C::G + base;
     const int qq = active ? q : 0;
     gr = qq / C::NBLK;
     gc0 = (qq % C::NBLK) * C::KB;
@@ -354,6 +368,53 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
   PHASE(10);
 }
 
+// One warp's EM-ADMM consensus for sweep t (XW = 1, 2): lane l owns coordinates 2l, 2l+1 and
+// sums their float2 column over the local group rows in a fixed order (8 interleaved chains,
+// then a tree); z_t = P_C(z - g/n), c = 2 z_t - z (admm.hpp:59-65 in p-form); flag bits 4
+// (non-finite z) and 8 (z != a0, only if the exact-stop test is possible) into flags[t & 1];
+// clears flags[(t+1) & 1] (every read of sweep t-1's word is done).
+template <class C, int NR>
+__device__ __forceinline__ void warp_consensus(TileCtx<C>& X, const float* rows, int t, float inv_n,
+                                               const nlem_box& range, bool static_eq) {
+  static_assert(C::GSTR % 2 == 0 && C::GSTR >= C::D + 1, "float2 coordinate pairs");
+  const int j = 2 * X.lane;
+  const bool own = j < C::D;
+  const float2* col = reinterpret_cast<const float2*>(rows + (own ? j : 0));
+  float2 ch[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ch[i] = make_float2(0.0f, 0.0f);
+#pragma unroll
+  for (int g = 0; g < NR; ++g) {
+    const float2 v = col[g * (C::GSTR / 2)];
+    ch[g % 8] = g < 8 ? v : __fadd2_rn(ch[g % 8], v);
+  }
+#pragma unroll
+  for (int w = 1; w < 8; w <<= 1)
+#pragma unroll
+    for (int i = 0; i + w < 8; i += 2 * w) ch[i] = __fadd2_rn(ch[i], ch[i + w]);
+  int f = 0;
+  if (own) {
+    const float gs[2] = {ch[0].x, ch[0].y};
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int jj = j + e;
+      if (jj < C::D) {
+        const float zo = X.z[jj];
+        const float zn = clamp_box(fmaf(-gs[e], inv_n, zo), range);
+        f |= isfinite(zn) ? 0 : 4;
+        if (static_eq) f |= (zn != X.a0[jj]) ? 8 : 0;
+        X.z[jj] = zn;
+        X.c2[jj] = tf2(2.0f * zn - zo);
+      }
+    }
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if (X.lane == 0) {
+    if (f) atomicOr(&X.flags[t & 1], f);
+    X.flags[(t + 1) & 1] = 0;
+  }
+}
+
 // IRLS consensus (CL == 1): lanes write their num partials v[dc] (coordinate j = dr*KS + dc)
 // and one lane per group writes the group's sum beta and sum w*root into columns D and D+1 of
 // the group row (GSTR >= D + 2).  CPT threads per coordinate sum the 3 columns over groups in
@@ -447,7 +508,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   int crank = 0;
   if constexpr (C::CL == 2) crank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
   X.carve(smem, crank);
-  (void)work_counter;
+  __shared__ long long s_next_chunk[2];  // CL == 1: this CTA's next chunk (double-buffered)
+  int chunk_parity = 0;
   constexpr int hs = C::SW / 2;
   constexpr int center = C::D / 2;
   const int64_t plane = out_rows * cols;
@@ -471,12 +533,22 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   }
   __syncthreads();
 
-  // static round-robin over pixel chunks per cluster (both CTAs of a cluster walk the same
-  // pixels; work per chunk is uniform up to the clipped image border)
+  // pixel chunks: CL == 1 takes chunk blockIdx.x, then grabs the next one from a global
+  // counter at the start of each chunk (dynamic, so a slow SM does not stretch the launch);
+  // a 2-CTA cluster walks a static round-robin so both CTAs see the same pixels
   const int64_t cid = blockIdx.x / C::CL, ncl = gridDim.x / C::CL;
   int64_t prefetched = -1;  // pixel whose tile is already in flight to smem
-  for (int64_t ch = cid; ch < nchunks; ch += ncl) {
+  for (int64_t ch = cid; ch < nchunks;) {
     const int64_t pix_end = (ch + 1) * chunk < plane ? (ch + 1) * chunk : plane;
+    if constexpr (C::CL == 1) {
+      // read after this chunk's first barrier; rewritten only after the chunk's last one
+      // (double-buffered: a slow reader of the previous slot can still be before its barrier)
+      if (X.tid == 0) s_next_chunk[chunk_parity] = ncl + atomicAdd(work_counter, 1);
+    }
+    const auto next_chunk = [&]() -> int64_t {
+      if constexpr (C::CL == 1) return s_next_chunk[chunk_parity];
+      return ch + ncl;
+    };
     for (int64_t pix = ch * chunk; pix < pix_end; ++pix) {
       const int64_t r = out_row0 + pix / cols, c = pix % cols;
       const int gr0 = r < hs ? static_cast<int>(hs - r) : 0;
@@ -512,6 +584,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         X.flags[0] = 0;
         X.flags[1] = 0;
         X.flags[2] = 0;
+        X.flags[3] = 0;  // consensus arrival counter (XW == 2)
       }
       // ---- segment registers
       Seg<C> S;
@@ -629,7 +702,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       // during the setup above, which ended with a barrier)
       {
         int64_t nxt = pix + 1;
-        if (nxt >= pix_end) nxt = (ch + ncl) * chunk < plane ? (ch + ncl) * chunk : -1;
+        if (nxt >= pix_end) nxt = next_chunk() < nchunks ? next_chunk() * chunk : -1;
         if (nxt >= 0) {
           const int64_t nr_ = out_row0 + nxt / cols, nc_ = nxt % cols;
           const float* nsrc = pad + (nr_ - out_row0) * pad_cols + nc_;
@@ -755,7 +828,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           __syncthreads();
         }
       }
-      if constexpr (C::XW == 1) {
+      if constexpr (C::XW >= 1) {
         if (P.solver == NLEM_SOLVER_ADMM) {
           // ---- EM-ADMM sweeps, split p-form with a dedicated consensus warp.  Between sweeps
           // a lane keeps q_k = s_k p_k - a_k; sweep t forms p_k = q_k + c (c = 2 z_{t-1} - z_{t-2}),
@@ -778,13 +851,14 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 #pragma unroll
             for (int dc = 0; dc < C::KS; ++dc) p1[dc] = C::ODD ? -S.single(dc) : 0.0f;
             float* red_row = X.red + (X.grow0 / C::G) * C::GSTR + X.dr * C::KS;
+            // c of the coming sweep, loaded as soon as it is published (before the flag checks)
+            float2 cc[C::KS];
+#pragma unroll
+            for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
             for (int t = 1; t <= P.iters; ++t) {
               WSTAMP(0);
               float nr[C::KB];
               {
-                float2 cc[C::KS];
-#pragma unroll
-                for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
 #pragma unroll
                 for (int qq = 0; qq < C::KP; ++qq) {
                   float2 acc = make_float2(0.0f, 0.0f);
@@ -832,25 +906,103 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
                 red_row[dc] = X.active ? tsum : 0.0f;
               }
-              fbits = __reduce_or_sync(0xffffffffu, fbits);
-              if (X.lane == 0 && fbits) atomicOr(&X.flags[t & 1], fbits);
+              if (fbits) atomicOr(&X.flags[t & 1], fbits);  // rare
               WSTAMP(1);
-              named_bar_arrive(1, C::THREADS);
-              // next sweep's q = s p - a, overlapping the consensus
+              // next sweep's q = s p - a (overlaps the consensus)
+              auto q_update = [&]() {
 #pragma unroll
-              for (int qq = 0; qq < C::KP; ++qq)
+                for (int qq = 0; qq < C::KP; ++qq)
 #pragma unroll
-                for (int dc = 0; dc < C::KS; ++dc) {
-                  const float2 a = S.pair(qq, dc);
-                  p2[qq][dc] = tfma2(s2[qq], p2[qq][dc], make_float2(-a.x, -a.y));
+                  for (int dc = 0; dc < C::KS; ++dc) {
+                    const float2 a = S.pair(qq, dc);
+                    p2[qq][dc] = tfma2(s2[qq], p2[qq][dc], make_float2(-a.x, -a.y));
+                  }
+                if (C::ODD) {
+#pragma unroll
+                  for (int dc = 0; dc < C::KS; ++dc) p1[dc] = fmaf(s1, p1[dc], -S.single(dc));
                 }
-              if (C::ODD) {
+              };
+              if constexpr (C::XW == 1) {
+                named_bar_arrive(1, C::THREADS);
+                q_update();
+                WSTAMP(2);
+                named_bar_sync(2, C::THREADS);
+              } else if constexpr (C::XW >= 3) {
+                // fold this warp's GPW group rows into its warp row (fixed order)
+                __syncwarp();
+                if (X.lane < (C::D + 1) / 2) {
+                  const float2* g0 =
+                      reinterpret_cast<const float2*>(X.red + X.warp * C::GPW * C::GSTR) + X.lane;
+                  float2 acc = g0[0];
 #pragma unroll
-                for (int dc = 0; dc < C::KS; ++dc) p1[dc] = fmaf(s1, p1[dc], -S.single(dc));
+                  for (int i = 1; i < C::GPW; ++i) acc = __fadd2_rn(acc, g0[i * (C::GSTR / 2)]);
+                  reinterpret_cast<float2*>(X.wred + X.warp * C::GSTR)[X.lane] = acc;
+                }
+                __syncthreads();
+                if constexpr (C::XW == 4) {
+                  // CPT threads per coordinate; loads first, then the state update, then the
+                  // fixed-order reduction (rows part, part + CPT, ...) and the finish
+                  constexpr int NPER = C::WARPS / C::CPT;
+                  const int j = X.tid / C::CPT, part = X.tid % C::CPT;
+                  const int jc = j < C::D ? j : 0;
+                  float lv[NPER];
+#pragma unroll
+                  for (int i = 0; i < NPER; ++i) lv[i] = X.wred[(part + i * C::CPT) * C::GSTR + jc];
+                  q_update();
+#pragma unroll
+                  for (int w = 1; w < NPER; w <<= 1)
+#pragma unroll
+                    for (int i = 0; i + w < NPER; i += 2 * w) lv[i] += lv[i + w];
+                  float gsum = lv[0];
+#pragma unroll
+                  for (int o = 1; o < C::CPT; o <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+                  if (j < C::D && part == 0) {
+                    const float zo = X.z[j];
+                    const float zn = clamp_box(fmaf(-gsum, inv_n, zo), P.range);
+                    int f = isfinite(zn) ? 0 : 4;
+                    if (static_eq) f |= (zn != X.a0[j]) ? 8 : 0;
+                    X.z[j] = zn;
+                    X.c2[j] = tf2(2.0f * zn - zo);
+                    if (f) atomicOr(&X.flags[t & 1], f);
+                    if (j == 0) X.flags[(t + 1) & 1] = 0;
+                  }
+                  WSTAMP(2);
+                  __syncthreads();
+                } else if (X.warp == C::WARPS - 1) {
+                  warp_consensus<C, C::WARPS>(X, X.wred, t, inv_n, P.range, static_eq);
+                  __syncwarp();
+                  named_bar_arrive(2, C::THREADS);
+                  q_update();
+                } else {
+                  q_update();
+                  WSTAMP(2);
+                  named_bar_sync(2, C::THREADS);
+                }
+              } else {
+                // arrival counter: the warp that hands in the last partials runs the consensus
+                // and releases the others (named barrier 2: they sync, it arrives)
+                __threadfence_block();
+                __syncwarp();
+                int old = 0;
+                if (X.lane == 0) old = atomicAdd(&X.flags[3], 1);
+                old = __shfl_sync(0xffffffffu, old, 0);
+                if (old == C::WARPS - 1) {
+                  __threadfence_block();
+                  warp_consensus<C, C::NGC>(X, X.red, t, inv_n, P.range, static_eq);
+                  if (X.lane == 0) X.flags[3] = 0;
+                  __threadfence_block();
+                  __syncwarp();
+                  named_bar_arrive(2, C::THREADS);
+                  q_update();
+                } else {
+                  q_update();
+                  WSTAMP(2);
+                  named_bar_sync(2, C::THREADS);
+                }
               }
-              WSTAMP(2);
-              named_bar_sync(2, C::THREADS);
               WSTAMP(3);
+#pragma unroll
+              for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
               const int fl = X.flags[t & 1];
 #ifdef NLEM_PHASE_PROFILE
               ++X.dbg_it;
@@ -868,53 +1020,12 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
               }
             }
           } else {
-            // consensus warp: lane l owns coordinates 2l, 2l+1; fixed-order sum over the groups
-            // (8 interleaved chains, then a tree), z_t = P_C(z - g/n), c = 2 z_t - z
-            const int j = 2 * X.lane;
-            const bool own = j < C::D;
-            const float2* col = reinterpret_cast<const float2*>(X.red + (own ? j : 0));
-            static_assert(C::GSTR % 2 == 0 && C::GSTR >= C::D + 1, "float2 coordinate pairs");
+            // dedicated consensus warp (XW == 1)
             for (int t = 1; t <= P.iters; ++t) {
               WSTAMP(0);
               named_bar_sync(1, C::THREADS);
               WSTAMP(1);
-              float2 ch[8];
-#pragma unroll
-              for (int i = 0; i < 8; ++i) ch[i] = make_float2(0.0f, 0.0f);
-#pragma unroll
-              for (int g = 0; g < C::NGC; ++g) {
-                const float2 v = col[g * (C::GSTR / 2)];
-                ch[g % 8].x += v.x;
-                ch[g % 8].y += v.y;
-              }
-#pragma unroll
-              for (int w = 1; w < 8; w <<= 1)
-#pragma unroll
-                for (int i = 0; i + w < 8; i += 2 * w) {
-                  ch[i].x += ch[i + w].x;
-                  ch[i].y += ch[i + w].y;
-                }
-              int f = 0;
-              if (own) {
-                const float gs[2] = {ch[0].x, ch[0].y};
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                  const int jj = j + e;
-                  if (jj < C::D) {
-                    const float zo = X.z[jj];
-                    const float zn = clamp_box(fmaf(-gs[e], inv_n, zo), P.range);
-                    f |= isfinite(zn) ? 0 : 4;
-                    if (static_eq) f |= (zn != X.a0[jj]) ? 8 : 0;
-                    X.z[jj] = zn;
-                    X.c2[jj] = tf2(2.0f * zn - zo);
-                  }
-                }
-              }
-              f = __reduce_or_sync(0xffffffffu, f);
-              if (X.lane == 0) {
-                if (f) atomicOr(&X.flags[t & 1], f);
-                X.flags[(t + 1) & 1] = 0;  // every read of sweep t-1's word is done
-              }
+              warp_consensus<C, C::NGC>(X, X.red, t, inv_n, P.range, static_eq);
               __syncwarp();
               const int fl = X.flags[t & 1];
               WSTAMP(2);
@@ -1056,6 +1167,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       }
       __syncthreads();
     }
+    ch = next_chunk();
+    chunk_parity ^= 1;
   }
   // no CTA may exit while its peer can still store into its shared memory
   if constexpr (C::CL == 2) cooperative_groups::this_cluster().sync();
@@ -1097,10 +1210,16 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
   const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (clusters * 4))));
   clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, (pixels + chunk - 1) / chunk));
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * C::CL));
-  e = cudaLaunchKernelEx(&cfg, kfn, L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P,
-                         L.out, L.frames, static_cast<int*>(nullptr), chunk, L.fail);
+  int* counter = nullptr;  // dynamic chunk counter (stream-ordered scratch)
+  e = cudaMallocAsync(&counter, sizeof(int), stream);
   if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
+  if (e == cudaSuccess)
+    e = cudaLaunchKernelEx(&cfg, kfn, L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows,
+                           L.P, L.out, L.frames, counter, chunk, L.fail);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  const cudaError_t ef = cudaFreeAsync(counter, stream);
+  return e != cudaSuccess ? e : ef;
 }
 
 }  // namespace
