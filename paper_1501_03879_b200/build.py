@@ -48,6 +48,10 @@ _VARIANT_TOKENS = {
     "xw2": "-DNLEM_TILE_XW=2",       # last-arriving warp runs the consensus
     "xw3": "-DNLEM_TILE_XW=3",       # warp pre-reduction + one consensus warp
     "xw4": "-DNLEM_TILE_XW=4",       # warp pre-reduction + CPT consensus, split p-form
+    "cpt1": "-DNLEM_XW4_CPT=1",      # XW=4 consensus threads per coordinate
+    "cpt2": "-DNLEM_XW4_CPT=2",
+    "cpt4": "-DNLEM_XW4_CPT=4",
+    "cpt8": "-DNLEM_XW4_CPT=8",
 }
 
 

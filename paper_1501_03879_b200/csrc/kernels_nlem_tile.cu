@@ -11,6 +11,8 @@
 // partials across the k lanes of the group, one prox scale per lane (rsqrt), a shuffle
 // broadcast, g partials, then one CTA barrier and a multi-thread consensus per coordinate.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -29,6 +31,11 @@ __device__ long long g_warp[32][64][4];  // per warp lane 0: sweep start, red wr
     if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && X.dbg_it < 64)                        \
       g_warp[threadIdx.x >> 5][X.dbg_it][slot] = clock64();                                 \
   } while (0)
+__device__ long long g_setup[64][8];  // thread 0 of CTA 0: per-pixel setup stamps
+#define SSTAMP(slot)                                                                          \
+  do {                                                                                       \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && X.dbg_px < 64) g_setup[X.dbg_px][slot] = clock64(); \
+  } while (0)
 #define PHASE(slot)                                                                            \
   do {                                                                                        \
     if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == blockDim.x - 32) && X.dbg_it < 64) \
@@ -41,8 +48,14 @@ __device__ long long g_warp[32][64][4];  // per warp lane 0: sweep start, red wr
 #define WSTAMP(slot) \
   do {               \
   } while (0)
+#define SSTAMP(slot) \
+  do {               \
+  } while (0)
 #endif
 
+#ifndef NLEM_XW4_CPT
+#define NLEM_XW4_CPT 8
+#endif
 template <int KS_, int SW_, int KB_, int CL_, int XW_ = 0>
 struct TileCfg {
   static constexpr int KS = KS_;                 // patch side k
@@ -64,6 +77,10 @@ struct TileCfg {
   // pre-reduction, then CPT threads per coordinate over the warp rows (all warps), with the
   // next sweep's state update issued between the consensus loads and their reduction
   static constexpr int XW = XW_;
+  // split-form paths (XW >= 1) publish c as KS padded rows of CSTR floats so a lane reads its
+  // patch row with 128-bit loads; CSTR/4 odd keeps the 7 row reads of a warp conflict-free
+  static constexpr int CSTR = (KS + 3) / 4 * 4 + ((((KS + 3) / 4) % 2) ? 0 : 4);
+  static constexpr int CSN = (KS * CSTR + 3) & ~3;
   static constexpr int THREADS = 32 * (WARPS + (XW == 1 ? 1 : 0));
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
@@ -90,7 +107,9 @@ struct TileCfg {
   static_assert(D <= THREADS, "consensus needs one thread per coordinate");
   static_assert(XW == 0 || (CL == 1 && D <= 64), "consensus warp: one CTA, <= 2 coordinates per lane");
   static_assert(XW != 2 || NGC <= 64, "arrival-counter consensus: 8 chains x 8 rows");
-  static_assert(XW != 4 || WARPS % CPT == 0, "warp rows split evenly over the CPT parts");
+  // XW == 4: threads per coordinate of the consensus over the WARPS warp rows
+  static constexpr int CPT4 = NLEM_XW4_CPT;
+  static_assert(XW != 4 || (WARPS % CPT4 == 0 && CPT4 * D <= THREADS), "warp rows split evenly");
 };
 
 // configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
@@ -115,7 +134,7 @@ struct TileSmem {
   static constexpr int NB = (ROWS * C::KBP + 3) & ~3;    // norm transpose (16-byte multiple)
   static constexpr int RED = ((C::NGC + 8 + C::WARPS) * C::GSTR + 3) & ~3;  // g partials per group
                                                    // (+ dummy groups) and per warp (XW >= 3)
-  static constexpr int TOTAL = 2 * T + NB + RED + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
+  static constexpr int TOTAL = 2 * T + NB + RED + C::CSN /*cs*/ + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
                                C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
                                4 /*mbarrier*/;
 };
@@ -201,6 +220,7 @@ struct TileCtx {
   float* red;   // [NGC + 8][GSTR] per-group g partials
   float* wred;  // [WARPS][GSTR] per-warp g partials (XW >= 3)
   float2* c2;   // [D]
+  float* cs;    // [KS][CSTR] c rows (XW >= 1)
   float* z;     // [D]
   float* a0;    // [D]
   float* wbuf;  // [NGROUPS][KBP]
@@ -216,13 +236,15 @@ struct TileCtx {
   int rank, nloc;  // CTA rank in the cluster, real groups held by this CTA
   int xpar = 0;    // cluster exchange parity (double-buffered receive buffers)
   int dbg_it = 0;  // debug phase-profile sweep counter
+  int dbg_px = 0;  // debug setup-profile pixel counter
   __device__ void carve(float* smem, int cta_rank) {
     T0 = smem;
     T1 = T0 + TileSmem<C>::T;
     nbuf = T1 + TileSmem<C>::T;
     red = nbuf + TileSmem<C>::NB;
     wred = red + (C::NGC + 8) * C::GSTR;
-    c2 = reinterpret_cast<float2*>(red + TileSmem<C>::RED);
+    cs = red + TileSmem<C>::RED;
+    c2 = reinterpret_cast<float2*>(cs + C::CSN);
     z = reinterpret_cast<float*>(c2 + C::D);
     a0 = z + C::D;
     wbuf = a0 + C::D;
@@ -404,7 +426,7 @@ __device__ __forceinline__ void warp_consensus(TileCtx<C>& X, const float* rows,
         f |= isfinite(zn) ? 0 : 4;
         if (static_eq) f |= (zn != X.a0[jj]) ? 8 : 0;
         X.z[jj] = zn;
-        X.c2[jj] = tf2(2.0f * zn - zo);
+        X.cs[(jj / C::KS) * C::CSTR + jj % C::KS] = 2.0f * zn - zo;
       }
     }
   }
@@ -559,6 +581,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       const float inv_n = 1.0f / static_cast<float>(n);
       // ---- tile (and its one-column-shifted copy) from the padded band; after the first
       // pixel it was prefetched with cp.async during the previous pixel's sweeps
+      SSTAMP(0);
       if (prefetched == pix) {
         cp_async_wait_all();
       } else {
@@ -596,7 +619,9 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 #pragma unroll
         for (int i = 0; i < C::NO; ++i) S.O[i] = pO[i];
       }
+      SSTAMP(1);
       const bool static_eq = !__syncthreads_or(neq);
+      SSTAMP(2);
       // is grid point m of my segment a real neighbour (inside the clipped window)?
       const bool row_real = X.active && X.gr >= gr0 && X.gr <= gr1;
       auto is_real = [&](int m) {
@@ -640,6 +665,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       }
       float wall[C::KB];
       group_broadcast<C>(X, wown, wall);
+      SSTAMP(3);
       // ---- initial patch (nlem.cpp:13-18)
       const bool nlm_init = P.solver == NLEM_SOLVER_NLM_ONLY || P.init_mode == NLEM_INIT_NLM_PATCH;
       bool init_done = false;
@@ -698,6 +724,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         __syncthreads();
       }
 
+      SSTAMP(4);
       // prefetch the next pixel's tile while this pixel's sweeps run (the tile is only read
       // during the setup above, which ended with a barrier)
       {
@@ -715,6 +742,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           prefetched = nxt;
         }
       }
+      SSTAMP(5);
       int iters = P.iters, fail_iter = -1, fail_kind = 0;
       if constexpr (C::CL == 1) {
         if (P.solver == NLEM_SOLVER_IRLS) {
@@ -836,7 +864,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           // with a non-blocking barrier arrive, and computes the next q while the consensus
           // warp reduces the partials and publishes z_t and c.  Same iterates as the p-form
           // (p' = s p + (c - a)) up to FP32 rounding order.
-          if (X.tid < C::D) X.c2[X.tid] = tf2(X.z[X.tid]);
+          if (X.tid < C::D) X.cs[(X.tid / C::KS) * C::CSTR + X.tid % C::KS] = X.z[X.tid];
           __syncthreads();
           if (X.warp < C::WARPS) {
             float lam_own[C::SPL];
@@ -851,10 +879,28 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 #pragma unroll
             for (int dc = 0; dc < C::KS; ++dc) p1[dc] = C::ODD ? -S.single(dc) : 0.0f;
             float* red_row = X.red + (X.grow0 / C::G) * C::GSTR + X.dr * C::KS;
-            // c of the coming sweep, loaded as soon as it is published (before the flag checks)
-            float2 cc[C::KS];
+            // c of the coming sweep (this lane's patch row), loaded as soon as it is published
+            // (before the flag checks) with 128-bit loads
+            float cc[C::CSTR];
+            const float4* crow = reinterpret_cast<const float4*>(X.cs + X.dr * C::CSTR);
+            auto load_c = [&]() {
 #pragma unroll
-            for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
+              for (int i = 0; i < (C::KS + 3) / 4; ++i) {
+                const float4 v = crow[i];
+                cc[4 * i] = v.x;
+                cc[4 * i + 1] = v.y;
+                cc[4 * i + 2] = v.z;
+                cc[4 * i + 3] = v.w;
+              }
+            };
+            load_c();
+            // XW == 4: the consensus thread of coordinate cj (part 0 of CPT4) keeps z_j and a0_j
+            const int cj = X.tid / C::CPT4, cpart = X.tid % C::CPT4;
+            const bool cfin = cj < C::D && cpart == 0;
+            const int cjc = cj < C::D ? cj : 0;
+            const int cidx = (cjc / C::KS) * C::CSTR + cjc % C::KS;
+            float zreg = X.z[cjc];
+            const float a0reg = X.a0[cjc];
             for (int t = 1; t <= P.iters; ++t) {
               WSTAMP(0);
               float nr[C::KB];
@@ -864,7 +910,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
                   for (int dc = 0; dc < C::KS; ++dc) {
-                    p2[qq][dc] = __fadd2_rn(p2[qq][dc], cc[dc]);
+                    p2[qq][dc] = __fadd2_rn(p2[qq][dc], tf2(cc[dc]));
                     acc = tfma2(p2[qq][dc], p2[qq][dc], acc);
                   }
                   nr[2 * qq] = acc.x;
@@ -874,7 +920,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   float acc = 0.0f;
 #pragma unroll
                   for (int dc = 0; dc < C::KS; ++dc) {
-                    p1[dc] += cc[dc].x;
+                    p1[dc] += cc[dc];
                     acc = fmaf(p1[dc], p1[dc], acc);
                   }
                   nr[C::KB - 1] = acc;
@@ -904,7 +950,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 for (int qq = 0; qq < C::KP; ++qq) acc = tfma2(s2[qq], p2[qq][dc], acc);
                 float tsum = acc.x + acc.y;
                 if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
-                red_row[dc] = X.active ? tsum : 0.0f;
+                red_row[dc] = tsum;  // idle lanes: s = 0 on finite p (lambda = 0) -> exact 0
               }
               if (fbits) atomicOr(&X.flags[t & 1], fbits);  // rare
               WSTAMP(1);
@@ -942,12 +988,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 if constexpr (C::XW == 4) {
                   // CPT threads per coordinate; loads first, then the state update, then the
                   // fixed-order reduction (rows part, part + CPT, ...) and the finish
-                  constexpr int NPER = C::WARPS / C::CPT;
-                  const int j = X.tid / C::CPT, part = X.tid % C::CPT;
-                  const int jc = j < C::D ? j : 0;
+                  constexpr int NPER = C::WARPS / C::CPT4;
                   float lv[NPER];
 #pragma unroll
-                  for (int i = 0; i < NPER; ++i) lv[i] = X.wred[(part + i * C::CPT) * C::GSTR + jc];
+                  for (int i = 0; i < NPER; ++i) lv[i] = X.wred[(cpart + i * C::CPT4) * C::GSTR + cjc];
                   q_update();
 #pragma unroll
                   for (int w = 1; w < NPER; w <<= 1)
@@ -955,16 +999,17 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                     for (int i = 0; i + w < NPER; i += 2 * w) lv[i] += lv[i + w];
                   float gsum = lv[0];
 #pragma unroll
-                  for (int o = 1; o < C::CPT; o <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
-                  if (j < C::D && part == 0) {
-                    const float zo = X.z[j];
+                  for (int o = 1; o < C::CPT4; o <<= 1) gsum += __shfl_xor_sync(0xffffffffu, gsum, o);
+                  if (cfin) {
+                    const float zo = zreg;
                     const float zn = clamp_box(fmaf(-gsum, inv_n, zo), P.range);
                     int f = isfinite(zn) ? 0 : 4;
-                    if (static_eq) f |= (zn != X.a0[j]) ? 8 : 0;
-                    X.z[j] = zn;
-                    X.c2[j] = tf2(2.0f * zn - zo);
+                    if (static_eq) f |= (zn != a0reg) ? 8 : 0;
+                    zreg = zn;
+                    X.z[cj] = zn;
+                    X.cs[cidx] = 2.0f * zn - zo;
                     if (f) atomicOr(&X.flags[t & 1], f);
-                    if (j == 0) X.flags[(t + 1) & 1] = 0;
+                    if (cj == 0) X.flags[(t + 1) & 1] = 0;
                   }
                   WSTAMP(2);
                   __syncthreads();
@@ -1001,8 +1046,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 }
               }
               WSTAMP(3);
-#pragma unroll
-              for (int dc = 0; dc < C::KS; ++dc) cc[dc] = X.c2[X.dr * C::KS + dc];
+              load_c();
               const int fl = X.flags[t & 1];
 #ifdef NLEM_PHASE_PROFILE
               ++X.dbg_it;
@@ -1152,6 +1196,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           }
         }
       }
+      SSTAMP(6);
+#ifdef NLEM_PHASE_PROFILE
+      ++X.dbg_px;
+#endif
       if (X.tid == 0 && X.rank == 0) {
         if (fail_iter >= 0) {
           record_failure(fail, r * cols + c, fail_iter, fail_kind);
@@ -1228,6 +1276,9 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
 }  // namespace nlemk
 extern "C" int nlem_debug_phase_times(long long* out /* [2][64][16] */) {
   return cudaMemcpyFromSymbol(out, nlemk::g_phase, sizeof(nlemk::g_phase)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int nlem_debug_setup_times(long long* out /* [64][8] */) {
+  return cudaMemcpyFromSymbol(out, nlemk::g_setup, sizeof(nlemk::g_setup)) == cudaSuccess ? 0 : 1;
 }
 extern "C" int nlem_debug_warp_times(long long* out /* [32][64][4] */) {
   return cudaMemcpyFromSymbol(out, nlemk::g_warp, sizeof(nlemk::g_warp)) == cudaSuccess ? 0 : 1;

@@ -44,7 +44,12 @@ def main():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     for rnd in range(2):  # two interleaved rounds: drift shows up as round-to-round change
         for v in args or [""]:
-            env = dict(os.environ, NLEM_LIB_VARIANT=v)
+            # "variant" or "variant:ENV=VALUE" (e.g. ":NLEM_NO_TMA=1" = production with TMA off)
+            lib_v, _, envs = v.partition(":")
+            env = dict(os.environ, NLEM_LIB_VARIANT=lib_v)
+            if envs:
+                k, _, val = envs.partition("=")
+                env[k] = val
             r = subprocess.run([sys.executable, "-c", CHILD % dict(root=root, reps=reps, rows=rows)],
                                env=env, capture_output=True, text=True, timeout=900)
             line = r.stdout.strip().splitlines()[-1] if r.stdout.strip() else r.stderr[-300:]

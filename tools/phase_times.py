@@ -45,6 +45,8 @@ for w in range(2):
         rows.append(seg + [nxt] + sub)
     a = np.array(rows[2:])  # skip warm-up sweeps
     print(f"warp {'0' if w == 0 else 'last'}: sweeps={len(a)}")
+    if len(a) == 0:
+        continue
     for k, n in enumerate(names):
         print(f"   {n:28s} mean {a[:, k].mean():8.1f}  median {np.median(a[:, k]):8.1f}")
     print(f"   total per sweep (median)     {np.median(a[:, :5].sum(1) + a[:, 5]):8.1f}")
@@ -65,3 +67,21 @@ med = np.median(a, axis=0)
 print("per-warp median cycles since the earliest sweep start (sweep start, red written, after B1, after B2, next start):")
 for w in range(nw):
     print(f"  warp {w:2d}: " + "  ".join(f"{x:7.0f}" for x in med[:, w]))
+
+sb = np.zeros((64, 8), np.int64)
+if hasattr(lib, "nlem_debug_setup_times") and lib.nlem_debug_setup_times(
+        sb.ctypes.data_as(C.POINTER(C.c_longlong))) == 0:
+    segs = ["tile wait+neq scan", "syncthreads_or", "weights+bcast", "init consensus", "prefetch issue",
+            "sweeps", "epilogue->next pixel"]
+    rows = []
+    for i in range(2, 62):
+        d = sb[i]
+        if (d[:7] == 0).any() or sb[i + 1, 0] == 0:
+            continue
+        rows.append([d[k + 1] - d[k] for k in range(6)] + [sb[i + 1, 0] - d[6]])
+    if rows:
+        a = np.array(rows)
+        print(f"per-pixel setup (thread 0, CTA 0; {len(a)} pixels), median cycles:")
+        for k, n in enumerate(segs):
+            print(f"   {n:24s} {np.median(a[:, k]):8.0f}")
+        print(f"   {'total per pixel':24s} {np.median(a.sum(1)):8.0f}")
