@@ -33,6 +33,14 @@ const DeviceCaps& device_caps() {
     cudaDeviceGetAttribute(&c.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaDeviceGetAttribute(&c.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
     cudaDeviceGetAttribute(&c.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    // the stream-ordered scratch (padded bands, counters) comes from the device's default pool:
+    // keep freed blocks mapped instead of trimming them at every synchronize, so the first call
+    // after a host sync does not pay for re-mapping
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t keep = ~uint64_t(0);
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     caps[dev] = c;
     have[dev] = true;
   }
@@ -400,6 +408,7 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
                               const nlem_params* params, float* out, float* frames,
                               nlem_failure* failure, void* stream, int nlm_ratio) {
   clear(failure);
+  (void)nlemk::device_caps();  // per-device setup (memory-pool policy) before the first allocation
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (rows < 1 || cols < 1) return invalid(failure, "image must be non-empty");  // image.hpp:15
   if (nlem_status st = validate_params_impl(params, failure)) return st;

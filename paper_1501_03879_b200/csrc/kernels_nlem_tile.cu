@@ -101,6 +101,9 @@ struct TileCfg {
   // are conflict-free; the consensus warp's float2 row reads are conflict-free for any stride)
   static constexpr int GSTR = (XW_ && D == 49) ? 56
                               : D == 49 ? 52 : ((D + 3) & ~3) + (((((D + 3) & ~3) / 4) % 2) ? 0 : 4);
+  // per-warp partial rows (XW >= 3): CPT4 = 8 threads read one coordinate from rows part, part+8,
+  // ...; a stride of 52 puts the 8 parts on distinct bank quads (56 collided parts p, p+4)
+  static constexpr int WSTR = D == 49 ? 52 : GSTR;
   static constexpr int SPL = (KB + G - 1) / G;   // points whose prox scale a lane computes
   static constexpr int CPT = THREADS >= 8 * D ? 8 : THREADS >= 4 * D ? 4 : THREADS >= 2 * D ? 2 : 1;
   static_assert(SW % KB == 0, "segments tile the grid row");
@@ -132,7 +135,7 @@ struct TileSmem {
   static constexpr int T = C::TH * C::TWS;            // one tile copy
   static constexpr int ROWS = C::NGC * C::G + 40;  // local groups + dummy rows for idle lanes
   static constexpr int NB = (ROWS * C::KBP + 3) & ~3;    // norm transpose (16-byte multiple)
-  static constexpr int RED = ((C::NGC + 8 + C::WARPS) * C::GSTR + 3) & ~3;  // g partials per group
+  static constexpr int RED = ((C::NGC + 8) * C::GSTR + C::WARPS * C::WSTR + 3) & ~3;  // g partials per group
                                                    // (+ dummy groups) and per warp (XW >= 3)
   static constexpr int TOTAL = 2 * T + NB + RED + C::CSN /*cs*/ + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
                                C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
@@ -231,6 +234,7 @@ struct TileCtx {
   int tid, warp, lane, q, dr, base;
   int grow0;    // first transpose/partial row of the lane's group (dummy rows if idle)
   bool active;  // lane belongs to a real group
+  bool slot;    // lane belongs to a group slot (lanes past GPW * G of a warp are idle)
   int gr, gc0;  // grid row and first grid column of the lane's segment
 
   int rank, nloc;  // CTA rank in the cluster, real groups held by this CTA
@@ -264,6 +268,7 @@ struct TileCtx {
     q = rank * C::NGC + lq;             // global group
     nloc = min(C::NGC, C::NGROUPS - rank * C::NGC);
     active = ql < C::GPW && lq < nloc;
+    slot = ql < C::GPW;
     // lanes of a group slot without a real group keep their slot's rows (all-zero partials, so
     // per-warp sums over GPW rows stay exact); lanes outside any slot get private dummy rows
     grow0 = ql < C::GPW ? lq * C::G : C::NGC * C::G + base;
@@ -291,14 +296,17 @@ __device__ __forceinline__ float tree_sum_col(const float* col, int stride) {
 template <class C>
 __device__ __forceinline__ void group_point_totals(TileCtx<C>& X, const float (&v)[C::KB],
                                                    float (&tot)[C::SPL]) {
+  // lanes outside a group slot skip the exchange: their dummy rows shared banks with real rows
   float* row = X.nbuf + (X.grow0 + X.dr) * C::KBP;
+  if (X.slot) {
 #pragma unroll
-  for (int m = 0; m < C::KB; ++m) row[m] = v[m];
+    for (int m = 0; m < C::KB; ++m) row[m] = v[m];
+  }
   __syncwarp();
 #pragma unroll
   for (int i = 0; i < C::SPL; ++i) {
     const int m = X.dr + i * C::G;
-    tot[i] = (C::SPL == 1 || m < C::KB)
+    tot[i] = X.slot && (C::SPL == 1 || m < C::KB)
                  ? tree_sum_col<C>(X.nbuf + X.grow0 * C::KBP + (m < C::KB ? m : 0), C::KBP)
                  : 0.0f;
   }
@@ -395,10 +403,10 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
 // then a tree); z_t = P_C(z - g/n), c = 2 z_t - z (admm.hpp:59-65 in p-form); flag bits 4
 // (non-finite z) and 8 (z != a0, only if the exact-stop test is possible) into flags[t & 1];
 // clears flags[(t+1) & 1] (every read of sweep t-1's word is done).
-template <class C, int NR>
+template <class C, int NR, int RSTR = C::GSTR>
 __device__ __forceinline__ void warp_consensus(TileCtx<C>& X, const float* rows, int t, float inv_n,
                                                const nlem_box& range, bool static_eq) {
-  static_assert(C::GSTR % 2 == 0 && C::GSTR >= C::D + 1, "float2 coordinate pairs");
+  static_assert(RSTR % 2 == 0 && RSTR >= C::D + 1, "float2 coordinate pairs");
   const int j = 2 * X.lane;
   const bool own = j < C::D;
   const float2* col = reinterpret_cast<const float2*>(rows + (own ? j : 0));
@@ -407,7 +415,7 @@ __device__ __forceinline__ void warp_consensus(TileCtx<C>& X, const float* rows,
   for (int i = 0; i < 8; ++i) ch[i] = make_float2(0.0f, 0.0f);
 #pragma unroll
   for (int g = 0; g < NR; ++g) {
-    const float2 v = col[g * (C::GSTR / 2)];
+    const float2 v = col[g * (RSTR / 2)];
     ch[g % 8] = g < 8 ? v : __fadd2_rn(ch[g % 8], v);
   }
 #pragma unroll
@@ -445,7 +453,7 @@ template <class C, class Finish>
 __device__ __forceinline__ void irls_reduce(TileCtx<C>& X, const float (&v)[C::KS], float gden,
                                             float gsur, Finish finish) {
   static_assert(C::GSTR >= C::D + 2, "room for the den / surrogate columns");
-  {
+  if (X.slot) {  // (lanes outside a group slot: dummy rows, never read)
     float* row = X.red + (X.grow0 / C::G) * C::GSTR;
 #pragma unroll
     for (int dc = 0; dc < C::KS; ++dc) row[X.dr * C::KS + dc] = v[dc];
@@ -950,7 +958,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 for (int qq = 0; qq < C::KP; ++qq) acc = tfma2(s2[qq], p2[qq][dc], acc);
                 float tsum = acc.x + acc.y;
                 if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
-                red_row[dc] = tsum;  // idle lanes: s = 0 on finite p (lambda = 0) -> exact 0
+                if (X.slot) red_row[dc] = tsum;  // idle slot lanes: s = 0 on finite p -> exact 0
               }
               if (fbits) atomicOr(&X.flags[t & 1], fbits);  // rare
               WSTAMP(1);
@@ -982,7 +990,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   float2 acc = g0[0];
 #pragma unroll
                   for (int i = 1; i < C::GPW; ++i) acc = __fadd2_rn(acc, g0[i * (C::GSTR / 2)]);
-                  reinterpret_cast<float2*>(X.wred + X.warp * C::GSTR)[X.lane] = acc;
+                  reinterpret_cast<float2*>(X.wred + X.warp * C::WSTR)[X.lane] = acc;
                 }
                 __syncthreads();
                 if constexpr (C::XW == 4) {
@@ -991,7 +999,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   constexpr int NPER = C::WARPS / C::CPT4;
                   float lv[NPER];
 #pragma unroll
-                  for (int i = 0; i < NPER; ++i) lv[i] = X.wred[(cpart + i * C::CPT4) * C::GSTR + cjc];
+                  for (int i = 0; i < NPER; ++i) lv[i] = X.wred[(cpart + i * C::CPT4) * C::WSTR + cjc];
                   q_update();
 #pragma unroll
                   for (int w = 1; w < NPER; w <<= 1)
@@ -1014,7 +1022,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   WSTAMP(2);
                   __syncthreads();
                 } else if (X.warp == C::WARPS - 1) {
-                  warp_consensus<C, C::WARPS>(X, X.wred, t, inv_n, P.range, static_eq);
+                  warp_consensus<C, C::WARPS, C::WSTR>(X, X.wred, t, inv_n, P.range, static_eq);
                   __syncwarp();
                   named_bar_arrive(2, C::THREADS);
                   q_update();
