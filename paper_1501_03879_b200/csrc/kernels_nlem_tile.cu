@@ -615,7 +615,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         X.flags[0] = 0;
         X.flags[1] = 0;
         X.flags[2] = 0;
-        X.flags[3] = 0;  // consensus arrival counter (XW == 2)
+        X.flags[3] = 0;           // consensus arrival counter (XW == 2)
+        X.flags[4] = 0x7fffffff;  // XW == 4: first failing sweep (2 t + [no non-finite z])
       }
       // ---- segment registers
       Seg<C> S;
@@ -960,7 +961,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 if (C::ODD) tsum = fmaf(s1, p1[dc], tsum);
                 if (X.slot) red_row[dc] = tsum;  // idle slot lanes: s = 0 on finite p -> exact 0
               }
-              if (fbits) atomicOr(&X.flags[t & 1], fbits);  // rare
+              if (fbits) {  // rare
+                atomicOr(&X.flags[t & 1], fbits);
+                if (C::XW == 4 && (fbits & 1)) atomicMin(&X.flags[4], 2 * t + 1);
+              }
               WSTAMP(1);
               // next sweep's q = s p - a (overlaps the consensus)
               auto q_update = [&]() {
@@ -1016,7 +1020,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                     zreg = zn;
                     X.z[cj] = zn;
                     X.cs[cidx] = 2.0f * zn - zo;
-                    if (f) atomicOr(&X.flags[t & 1], f);
+                    if (f) {
+                      atomicOr(&X.flags[t & 1], f);
+                      if (f & 4) atomicMin(&X.flags[4], 2 * t);
+                    }
                     if (cj == 0) X.flags[(t + 1) & 1] = 0;
                   }
                   WSTAMP(2);
@@ -1055,20 +1062,46 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
               }
               WSTAMP(3);
               load_c();
-              const int fl = X.flags[t & 1];
 #ifdef NLEM_PHASE_PROFILE
               ++X.dbg_it;
 #endif
-              if (fl & (4 | 1)) {
-                fail_iter = (fl & 4) || t == 1 ? t : t - 1;
-                fail_kind = NLEM_FAIL_ADMM_ITERATE;
-                break;
+              if constexpr (C::XW == 4) {
+                // failures are recorded as the first failing sweep (flags[4]) and decoded after
+                // the loop: no per-sweep flag read or divergent branch on the critical path; the
+                // flag word is read only when the exact-stop test is possible (constant footprint)
+                if (frames != nullptr) {
+                  if (X.tid == 0) frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
+                }
+                if (static_eq) {
+                  const int fl = X.flags[t & 1];
+                  if (!(fl & (4 | 1 | 2 | 8)) && X.flags[4] == 0x7fffffff) {  // residual exactly 0
+                    iters = t;
+                    break;
+                  }
+                }
+              } else {
+                const int fl = X.flags[t & 1];
+                if (fl & (4 | 1)) {
+                  fail_iter = (fl & 4) || t == 1 ? t : t - 1;
+                  fail_kind = NLEM_FAIL_ADMM_ITERATE;
+                  break;
+                }
+                if (frames && X.tid == 0)
+                  frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
+                if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
+                  iters = t;
+                  break;
+                }
               }
-              if (frames && X.tid == 0)
-                frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
-              if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
-                iters = t;
-                break;
+            }
+            if constexpr (C::XW == 4) {
+              // decode the first failure: non-finite z at sweep t -> t; a non-finite norm at
+              // sweep t (multiplier blow-up in t - 1) -> t - 1, or t for t = 1
+              const int fw = X.flags[4];
+              if (fw != 0x7fffffff) {
+                const int tf = fw >> 1;
+                fail_iter = !(fw & 1) || tf == 1 ? tf : tf - 1;
+                fail_kind = NLEM_FAIL_ADMM_ITERATE;
               }
             }
           } else {

@@ -333,3 +333,22 @@ def test_optimality_certificate(nb, oracle):
     # a non-optimal point has a clearly positive residual
     bad = nb.optimality_residual(pts, w, np.full((B, d), 0.9, np.float32))
     assert (bad > 1e-2).all()
+
+
+@pytest.mark.gpu
+def test_tile_kernel_admm_failure_reports_pixel_and_iteration(nb):
+    """k=7/S=21 (tile kernel, production consensus path): a float overflow in the sweep is a
+    NumericFailure naming the lowest failing pixel and the iteration (test_denoise.cpp:323-338
+    semantics at float range; the FP64 oracle does not overflow on these values)."""
+    img = np.zeros((30, 30), np.float32)
+    img[12:18, 12:18] = np.where(np.add.outer(np.arange(6), np.arange(6)) % 2 == 0, 0.0, 3e19)
+    p = nb.NlemParams(search=21, patch=7, h=1e30, sigma=10.0, solver="admm", solver_iters=4,
+                      mu=1.0, range=nb.BoxConstraint.unconstrained())
+    with pytest.raises(nb.NumericFailure) as e:
+        nb.nlem_denoise(img, p)
+    msg = str(e.value)
+    assert "pixel (" in msg and "iteration" in msg, msg
+    # deterministic: the same failure on a repeat run
+    with pytest.raises(nb.NumericFailure) as e2:
+        nb.nlem_denoise(img, p)
+    assert str(e2.value) == msg
