@@ -450,11 +450,23 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
-    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=seg2|tile|fast|generic
+    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=lr|seg2|tile|fast|generic
     // forces one (A/B measurements; falls back to generic when unsupported)
     static const char* force = std::getenv("NLEM_KERNEL");
     const std::string k = force ? force : "";
-    if ((k.empty() || k == "tile") && nlem_tile_supported(L)) e = launch_nlem_tile(L, s);
+    if ((k.empty() || k == "lr") && nlem_lr_supported(L)) {
+      // low-rank kernel, then the exact tile kernel over the pixels it handed off
+      int* scratch = nullptr;  // [0] work counter, [1] hand-off count, [2..] hand-off list
+      const int64_t pixels = out_rows * cols;
+      e = cudaMallocAsync(&scratch, (2 + pixels) * sizeof(int), s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int), s);
+      if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 2, scratch + 1, scratch, s);
+      if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 2, scratch + 1, s);
+      if (scratch) {
+        const cudaError_t ef = cudaFreeAsync(scratch, s);
+        if (e == cudaSuccess) e = ef;
+      }
+    } else if ((k.empty() || k == "tile") && nlem_tile_supported(L)) e = launch_nlem_tile(L, s);
     else if ((k.empty() || k == "seg2") && nlem_seg2_supported(L)) e = launch_nlem_seg2(L, s);
     else if ((k.empty() || k == "fast") && nlem_fast_supported(L)) e = launch_nlem_fast(L, s);
     else e = launch_nlem_generic(L, s);

@@ -532,7 +532,8 @@ template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::CL)
 nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
                  int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
-                 int* work_counter, int chunk, FailureSlot* fail) {
+                 int* work_counter, int chunk, FailureSlot* fail, const int* list,
+                 const int* list_count) {
   extern __shared__ __align__(16) float smem[];
   TileCtx<C> X;
   int crank = 0;
@@ -543,7 +544,10 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   constexpr int hs = C::SW / 2;
   constexpr int center = C::D / 2;
   const int64_t plane = out_rows * cols;
-  const int64_t nchunks = (plane + chunk - 1) / chunk;
+  // list mode: only the listed band pixels (the low-rank kernel's hand-offs), in list order
+  const int64_t npix = list ? static_cast<int64_t>(*list_count) : plane;
+  const int64_t nchunks = (npix + chunk - 1) / chunk;
+  auto pixel_at = [&](int64_t q) -> int64_t { return list ? static_cast<int64_t>(list[q]) : q; };
   const float inv_mu = 1.0f / P.mu;
   // lane-constant tile addressing of the segment (row gr+dr, columns gc0..gc0+SEG)
   const int trow = X.gr + X.dr;
@@ -569,7 +573,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   const int64_t cid = blockIdx.x / C::CL, ncl = gridDim.x / C::CL;
   int64_t prefetched = -1;  // pixel whose tile is already in flight to smem
   for (int64_t ch = cid; ch < nchunks;) {
-    const int64_t pix_end = (ch + 1) * chunk < plane ? (ch + 1) * chunk : plane;
+    const int64_t q_end = (ch + 1) * chunk < npix ? (ch + 1) * chunk : npix;
     if constexpr (C::CL == 1) {
       // read after this chunk's first barrier; rewritten only after the chunk's last one
       // (double-buffered: a slow reader of the previous slot can still be before its barrier)
@@ -579,7 +583,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       if constexpr (C::CL == 1) return s_next_chunk[chunk_parity];
       return ch + ncl;
     };
-    for (int64_t pix = ch * chunk; pix < pix_end; ++pix) {
+    for (int64_t q = ch * chunk; q < q_end; ++q) {
+      const int64_t pix = pixel_at(q);
       const int64_t r = out_row0 + pix / cols, c = pix % cols;
       const int gr0 = r < hs ? static_cast<int>(hs - r) : 0;
       const int gr1 = rows - 1 - r < hs ? static_cast<int>(hs + (rows - 1 - r)) : C::SW - 1;
@@ -737,8 +742,9 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       // prefetch the next pixel's tile while this pixel's sweeps run (the tile is only read
       // during the setup above, which ended with a barrier)
       {
-        int64_t nxt = pix + 1;
-        if (nxt >= pix_end) nxt = next_chunk() < nchunks ? next_chunk() * chunk : -1;
+        int64_t nq = q + 1;
+        if (nq >= q_end) nq = next_chunk() < nchunks ? next_chunk() * chunk : -1;
+        const int64_t nxt = nq >= 0 ? pixel_at(nq) : -1;
         if (nxt >= 0) {
           const int64_t nr_ = out_row0 + nxt / cols, nc_ = nxt % cols;
           const float* nsrc = pad + (nr_ - out_row0) * pad_cols + nc_;
@@ -1266,7 +1272,8 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 namespace {
 
 template <class C>
-cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
+cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream, const int* list = nullptr,
+                        const int* list_count = nullptr) {
   const size_t smem = TileSmem<C>::TOTAL * sizeof(float);
   auto kfn = nlem_pixels_tile<C>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1296,7 +1303,7 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
     clusters = int64_t(device_caps().sms) * std::max(per_sm, 1);
   }
-  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (clusters * 4))));
+  const int chunk = list ? 1 : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (clusters * 4))));
   clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, (pixels + chunk - 1) / chunk));
   cfg.gridDim = dim3(static_cast<unsigned>(clusters * C::CL));
   int* counter = nullptr;  // dynamic chunk counter (stream-ordered scratch)
@@ -1305,7 +1312,7 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream) {
   e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
   if (e == cudaSuccess)
     e = cudaLaunchKernelEx(&cfg, kfn, L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows,
-                           L.P, L.out, L.frames, counter, chunk, L.fail);
+                           L.P, L.out, L.frames, counter, chunk, L.fail, list, list_count);
   if (e == cudaSuccess) e = cudaGetLastError();
   const cudaError_t ef = cudaFreeAsync(counter, stream);
   return e != cudaSuccess ? e : ef;
@@ -1335,6 +1342,12 @@ bool nlem_tile_supported(const NlemLaunch& L) {
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream) {
   if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream);
   return launch_tile<TileK5S11>(L, stream);
+}
+
+cudaError_t launch_nlem_tile_list(const NlemLaunch& L, const int* list, const int* list_count,
+                                  cudaStream_t stream) {
+  if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream, list, list_count);
+  return launch_tile<TileK5S11>(L, stream, list, list_count);
 }
 
 }  // namespace nlemk

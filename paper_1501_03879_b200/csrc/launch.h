@@ -90,7 +90,15 @@ bool nlem_seg2_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_seg2(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);
+// tile kernel over a device-side list of band pixel indices (count read on the device)
+cudaError_t launch_nlem_tile_list(const NlemLaunch& L, const int* list, const int* list_count,
+                                  cudaStream_t stream);
 bool nlem_fast_supported(const NlemLaunch& L);
+// Low-rank (Gram-form) one-pixel-per-warp kernel (kernels_nlem_lr.cu): pixels whose history
+// ring would drop a significant term are appended to ovf_list for the tile kernel.
+bool nlem_lr_supported(const NlemLaunch& L);
+cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
+                           cudaStream_t stream);
 cudaError_t launch_nlem_fast(const NlemLaunch& L, cudaStream_t stream);
 
 cudaError_t launch_frames_sse(const float* frames, const float* clean, int64_t nframes,
