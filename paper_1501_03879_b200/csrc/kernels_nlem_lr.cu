@@ -53,14 +53,21 @@ constexpr int WARPS = 16;
 constexpr int SEGL = 7;  // points per segment
 constexpr int R = 4;     // history ring
 constexpr int NF = 8;    // state fields per point in TMEM
+#ifndef NLEM_LR_NPB
+#define NLEM_LR_NPB 1
+#endif
+constexpr int NPB = NLEM_LR_NPB;  // points per TMEM load/store in the scalar phase
 constexpr int RED_STR = 36;
 constexpr int CB_STR = 8;
 // per-warp shared memory (floats)
 constexpr int W_TILE0 = 0;
 constexpr int W_RED = 2 * TILE;
 constexpr int W_CB = W_RED + 32 * RED_STR;
-constexpr int W_TOTAL = W_CB + KS * CB_STR;
+constexpr int W_OWN = W_CB + KS * CB_STR;         // [4 + 2 (R+1)][32] owner scalars
+constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 ring
+constexpr int W_TOTAL = W_NR + 8;
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
+constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
 constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
@@ -77,39 +84,57 @@ __device__ __forceinline__ float rsq(float x) {
   return y;
 }
 
-// ---- TMEM (tcgen05) helpers: 32 lanes x 8 columns of 32-bit per warp access
-__device__ __forceinline__ void tm_ld8(uint32_t taddr, float (&v)[8]) {
-  uint32_t r0, r1, r2, r3, r4, r5, r6, r7;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3), "=r"(r4), "=r"(r5), "=r"(r6), "=r"(r7)
-               : "r"(taddr));
-  v[0] = __uint_as_float(r0);
-  v[1] = __uint_as_float(r1);
-  v[2] = __uint_as_float(r2);
-  v[3] = __uint_as_float(r3);
-  v[4] = __uint_as_float(r4);
-  v[5] = __uint_as_float(r5);
-  v[6] = __uint_as_float(r6);
-  v[7] = __uint_as_float(r7);
+// ---- TMEM (tcgen05) helpers: 32 lanes x N columns of 32-bit per warp access.  Each load is
+// issued together with its wait in one asm statement, so no use of the destination registers
+// can be scheduled before the data has landed (the loads are asynchronous).
+template <int N>
+__device__ __forceinline__ void tm_ld_wait(uint32_t taddr, float* v);
+template <>
+__device__ __forceinline__ void tm_ld_wait<8>(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
-// Completes all outstanding tcgen05.ld of this thread; the "+f" ties keep every use of the
-// loaded registers after the wait (the loads are asynchronous).
-__device__ __forceinline__ void tm_wait_ld(float (&v)[8]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]),
-                 "+f"(v[7])::"memory");
+template <>
+__device__ __forceinline__ void tm_ld_wait<16>(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void tm_tie(float (&v)[8]) {
-  asm volatile(""
-               : "+f"(v[0]), "+f"(v[1]), "+f"(v[2]), "+f"(v[3]), "+f"(v[4]), "+f"(v[5]), "+f"(v[6]),
-                 "+f"(v[7])::"memory");
-}
-__device__ __forceinline__ void tm_st8(uint32_t taddr, const float (&v)[8]) {
+template <int N>
+__device__ __forceinline__ void tm_st(uint32_t taddr, const float* v);
+template <>
+__device__ __forceinline__ void tm_st<8>(uint32_t taddr, const float* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
       "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
       "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
       "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void tm_st<16>(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
       : "memory");
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -151,15 +176,17 @@ __device__ __forceinline__ float row_sum(const float* row) {
 using namespace lr;
 
 __global__ void __launch_bounds__(WARPS * 32, 1)
-nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
-               int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
-               int* work_counter, int* ovf_list, int* ovf_count, FailureSlot* fail) {
+nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, int out_row0,
+               int plane, NlemDevParams P, float* out, float* frames, int* work_counter,
+               int* ovf_list, int* ovf_count, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* tm_base_slot = reinterpret_cast<uint32_t*>(smem + WARPS * W_TOTAL);
-  float* W = smem + warp * W_TOTAL;
-  float* red = W + W_RED;
-  float* cb = W + W_CB;
+  float* const W = smem + warp * W_TOTAL;
+  float* const red = W + W_RED;
+  float* const cb = W + W_CB;
+  float* const own = W + W_OWN + lane;  // owner scalars, row stride 32 (lane-private column)
+  float* const nrs = W + W_NR;          // ||c~||^2 history ring (warp-uniform)
 
   // ---- TMEM: all 512 columns for this CTA (1 CTA per SM by shared-memory size)
   if (warp == 0) {
@@ -176,191 +203,193 @@ nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, in
   auto t_pt = [&](int slot, int i) { return tw + static_cast<uint32_t>((slot * SEGL + i) * NF); };
   auto t_lam = [&](int slot) { return tw + static_cast<uint32_t>(112 + slot * 8); };
 
-  // lane geometry
-  int sgx[2], sgy0[2];
-  bool svalid[2];
-  seg_of(lane, 0, sgx[0], sgy0[0], svalid[0]);
-  seg_of(lane, 1, sgx[1], sgy0[1], svalid[1]);
-  const bool own1 = lane < D - 32;  // second owned coordinate j = 32 + lane
-  const int j0 = lane, j1 = own1 ? 32 + lane : 0;
+  // lane geometry: segment column offsets in the tile
+  int sgx0, sgy00, sgx1, sgy01;
+  bool sval0, sval1;
+  seg_of(lane, 0, sgx0, sgy00, sval0);
+  seg_of(lane, 1, sgx1, sgy01, sval1);
+  const int soff0 = sgy00 * TWS + sgx0, soff1 = sgy01 * TWS + sgx1;
+  // coordinate owners: the reduction runs in two halves (patch columns 0-3 and 4-6); row
+  // l of half A is coordinate (l % 7, l / 7), row l of half B is (l % 7, 4 + l / 7)
+  const bool own0 = lane < 4 * KS, own1 = lane < 3 * KS;
+  const int jy0 = lane % KS, jx0 = lane / KS, jx1 = 4 + lane / KS;
 
-  const int64_t plane = out_rows * cols;
   const float inv_mu = 1.0f / P.mu;
   const bool nlm_init = P.init_mode == NLEM_INIT_NLM_PATCH;
   const int total_warps = gridDim.x * WARPS;
 
-  int64_t pix = static_cast<int64_t>(blockIdx.x) * WARPS + warp;
+  int pix = blockIdx.x * WARPS + warp;
   int buf = 0;
-  auto issue_tile = [&](int64_t p, int b) {
-    const int64_t r = out_row0 + p / cols, c = p % cols;
-    const float* src = pad + (r - out_row0) * pad_cols + c;
-    float* T = W + W_TILE0 + b * TILE;
-    for (int e = lane; e < TH * TH; e += 32) {
-      const int tr = e / TH, tc = e - tr * TH;
-      cpa4(T + tr * TWS + tc, src + tr * pad_cols + tc);
+  auto issue_tile = [&](int p, int b) {
+    const int r = out_row0 + p / cols, c = p % cols;
+    const float* src = pad + static_cast<int64_t>(r - out_row0) * pad_cols + c;
+    float* T = W + b * TILE;
+    if (lane < TH) {  // one tile column per lane, row by row (no hoisted per-element offsets)
+#pragma unroll 1
+      for (int tr = 0; tr < TH; ++tr, src += pad_cols) cpa4(T + tr * TWS + lane, src + lane);
     }
     cpa_commit();
   };
   if (pix < plane) issue_tile(pix, 0);
 
   while (pix < plane) {
-    int64_t nxt = 0;
-    if (lane == 0) nxt = static_cast<int64_t>(atomicAdd(work_counter, 1)) + total_warps;
+    int nxt = 0;
+    if (lane == 0) nxt = atomicAdd(work_counter, 1) + total_warps;
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
     cpa_wait();
     __syncwarp();
-    const float* T = W + W_TILE0 + buf * TILE;
+    const float* const T = W + buf * TILE;
     if (nxt < plane) issue_tile(nxt, buf ^ 1);
 
-    const int64_t r = out_row0 + pix / cols, c = pix % cols;
-    const int gr0 = r < HS ? static_cast<int>(HS - r) : 0;
-    const int gr1 = rows - 1 - r < HS ? static_cast<int>(HS + (rows - 1 - r)) : SW - 1;
-    const int gc0 = c < HS ? static_cast<int>(HS - c) : 0;
-    const int gc1 = cols - 1 - c < HS ? static_cast<int>(HS + (cols - 1 - c)) : SW - 1;
-    const int n = (gr1 - gr0 + 1) * (gc1 - gc0 + 1);
-    const float inv_n = 1.0f / static_cast<float>(n);
+    const int r = out_row0 + pix / cols, c = pix % cols;
+    const int gr0 = r < HS ? HS - r : 0;
+    const int gr1 = rows - 1 - r < HS ? HS + (rows - 1 - r) : SW - 1;
+    const int gc0 = c < HS ? HS - c : 0;
+    const int gc1 = cols - 1 - c < HS ? HS + (cols - 1 - c) : SW - 1;
+    const float inv_n = 1.0f / static_cast<float>((gr1 - gr0 + 1) * (gc1 - gc0 + 1));
 
-    // ---- footprint constancy (exact-stop candidate, admm.hpp:77 with tol 0) and a0
-    const float ref = T[gr0 * TWS + gc0];
+    // ---- footprint constancy (exact-stop candidate, admm.hpp:77 with tol 0)
+    const float a0 = T[gr0 * TWS + gc0];
     bool neq = false;
-    for (int e = lane; e < TH * TH; e += 32) {
-      const int tr = e / TH, tc = e - tr * TH;
-      if (tr >= gr0 && tr <= gr1 + KS - 1 && tc >= gc0 && tc <= gc1 + KS - 1)
-        neq |= T[tr * TWS + tc] != ref;
+    if (lane >= gc0 && lane <= gc1 + KS - 1) {
+#pragma unroll 1
+      for (int tr = gr0; tr <= gr1 + KS - 1; ++tr) neq |= T[tr * TWS + lane] != a0;
     }
     const bool static_eq = !__any_sync(0xffffffffu, neq);
 
-    // ---- self patch m = a_self (grid point (HS, HS)); owners keep m_j
-    const float m0 = T[(HS + j0 / KS) * TWS + HS + j0 % KS];
-    const float m1 = T[(HS + j1 / KS) * TWS + HS + j1 % KS];
-
-    // ---- distances ||a_k - a_self||^2 (patch.cpp:52-61), weights, lambdas
-    float A2[2][SEGL];
-    {
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) A2[s][i] = 0.0f;
-        const float* col = T + sgy0[s] * TWS + sgx[s];
-#pragma unroll 1
-        for (int jx = 0; jx < KS; ++jx) {
-          float v[SEGL + KS - 1], ac[KS];
-#pragma unroll
-          for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS + jx];
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy) ac[jy] = T[(HS + jy) * TWS + HS + jx];
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy)
-#pragma unroll
-            for (int i = 0; i < SEGL; ++i) {
-              const float df = v[i + jy] - ac[jy];
-              A2[s][i] = fmaf(df, df, A2[s][i]);
-            }
-        }
-      }
-    }
-    float wgt[2][SEGL];
+    // ---- distances ||a_k - a_self||^2 (patch.cpp:52-61), weights, lambdas; state init
     unsigned realmask = 0;  // bit s*7+i: grid point inside the clipped window (patch.cpp:72-76)
+    float wgt[2][SEGL];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      const int gx = sgx[s];
-      const bool colreal = svalid[s] && gx >= gc0 && gx <= gc1;
+      float A2[SEGL];
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) A2[i] = 0.0f;
+      const float* col = T + (s ? soff1 : soff0);
+#pragma unroll 1
+      for (int jx = 0; jx < KS; ++jx) {
+        float v[SEGL + KS - 1], ac[KS];
+#pragma unroll
+        for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS + jx];
+#pragma unroll
+        for (int jy = 0; jy < KS; ++jy) ac[jy] = T[(HS + jy) * TWS + HS + jx];
+#pragma unroll
+        for (int jy = 0; jy < KS; ++jy)
+#pragma unroll
+          for (int i = 0; i < SEGL; ++i) {
+            const float df = v[i + jy] - ac[jy];
+            A2[i] = fmaf(df, df, A2[i]);
+          }
+      }
+      const int gx = s ? sgx1 : sgx0, gy0 = s ? sgy01 : sgy00;
+      const bool colreal = (s ? sval1 : sval0) && gx >= gc0 && gx <= gc1;
+      float lm[8];
 #pragma unroll
       for (int i = 0; i < SEGL; ++i) {
-        const int gy = sgy0[s] + i;
-        const bool real = colreal && gy >= gr0 && gy <= gr1;
-        wgt[s][i] = real ? expf(-A2[s][i] * P.inv_h2) : 0.0f;
+        const bool real = colreal && gy0 + i >= gr0 && gy0 + i <= gr1;
+        wgt[s][i] = real ? expf(-A2[i] * P.inv_h2) : 0.0f;
         realmask |= real ? 1u << (s * SEGL + i) : 0u;
+        lm[i] = inv_mu * wgt[s][i];
+        // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0
+        const float st[8] = {A2[i], -A2[i], 0.0f, A2[i], 0.0f, 0.0f, 0.0f, 0.0f};
+        tm_st<8>(t_pt(s, i), st);
       }
-    }
-    // state init in TMEM: H = ||a~||^2, K = -||a~||^2, ga = 0, A2, al = 0; lambdas
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-#pragma unroll
-      for (int i = 0; i < SEGL; ++i) {
-        const float st[8] = {A2[s][i], -A2[s][i], 0.0f, A2[s][i], 0.0f, 0.0f, 0.0f, 0.0f};
-        tm_st8(t_pt(s, i), st);
-      }
-      const float lm[8] = {inv_mu * wgt[s][0], inv_mu * wgt[s][1], inv_mu * wgt[s][2],
-                           inv_mu * wgt[s][3], inv_mu * wgt[s][4], inv_mu * wgt[s][5],
-                           inv_mu * wgt[s][6], 0.0f};
-      tm_st8(t_lam(s), lm);
+      lm[7] = 0.0f;
+      tm_st<8>(t_lam(s), lm);
     }
 
     // ---- patch-sum pass (sum_k u_k a_k per coordinate) + transpose reduction to the owners.
-    // rows: 0..48 coordinates, 49 sum u, 50..53 extra per-lane scalars
-    auto patch_sum_reduce = [&](const float (&u)[2][SEGL], const float (&extra)[5], float& own0,
-                                float& own1v, float (&xs)[5]) {
-      float g[D];
+    // Half A rows (jx - 0) * 7 + jy, half B rows (jx - 4) * 7 + jy, then 5 extra scalars.
+    auto patch_sum_reduce = [&](const float (&u)[2][SEGL], const float (&extra)[5], float& oA,
+                                float& oB, float (&xs)[5]) {
 #pragma unroll
-      for (int j = 0; j < D; ++j) g[j] = 0.0f;
+      for (int hf = 0; hf < 2; ++hf) {
+        const int jxa = hf ? 4 : 0, jxb = hf ? KS : 4;
+#pragma unroll 1
+        for (int jx = jxa; jx < jxb; ++jx) {
+          float gc[KS];
 #pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        const float* col = T + sgy0[s] * TWS + sgx[s];
+          for (int jy = 0; jy < KS; ++jy) gc[jy] = 0.0f;
 #pragma unroll
-        for (int jx = 0; jx < KS; ++jx) {
-          float v[SEGL + KS - 1];
+          for (int s = 0; s < 2; ++s) {
+            const float* col = T + (s ? soff1 : soff0) + jx;
+            float v[SEGL + KS - 1];
 #pragma unroll
-          for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS + jx];
+            for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS];
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy)
+            for (int jy = 0; jy < KS; ++jy)
 #pragma unroll
-            for (int i = 0; i < SEGL; ++i) g[jy * KS + jx] = fmaf(u[s][i], v[i + jy], g[jy * KS + jx]);
+              for (int i = 0; i < SEGL; ++i) gc[jy] = fmaf(u[s][i], v[i + jy], gc[jy]);
+          }
+          float* rrow = red + (jx - jxa) * KS * RED_STR + lane;
+#pragma unroll
+          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = gc[jy];
+        }
+        if (hf) {
+#pragma unroll
+          for (int q = 0; q < 5; ++q) red[(3 * KS + q) * RED_STR + lane] = extra[q];
+        }
+        __syncwarp();
+        float rr = 0.0f;
+        if (lane < (hf ? 3 * KS + 5 : 4 * KS)) rr = row_sum(red + lane * RED_STR);
+        __syncwarp();
+        if (hf == 0) {
+          oA = rr;
+        } else {
+          oB = rr;
+#pragma unroll
+          for (int q = 0; q < 5; ++q) xs[q] = __shfl_sync(0xffffffffu, rr, 3 * KS + q);
         }
       }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) red[j * RED_STR + lane] = g[j];
-      __syncwarp();
-      own0 = row_sum(red + lane * RED_STR);
-      __syncwarp();
-#pragma unroll
-      for (int j = 32; j < D; ++j) red[(j - 32) * RED_STR + lane] = g[j];
-#pragma unroll
-      for (int q = 0; q < 5; ++q) red[(D - 32 + q) * RED_STR + lane] = extra[q];
-      __syncwarp();
-      float rb = 0.0f;
-      if (lane < D - 32 + 5) rb = row_sum(red + lane * RED_STR);
-      __syncwarp();
-      own1v = rb;
-#pragma unroll
-      for (int q = 0; q < 5; ++q) xs[q] = __shfl_sync(0xffffffffu, rb, D - 32 + q);
     };
 
-    // ---- initial patch (nlem.cpp:13-18): weighted mean (ratio form) or the noisy patch
-    float z0, z1;
-    if (nlm_init) {
-      float ex[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+    // ---- initial patch (nlem.cpp:13-18): weighted mean (ratio form) or the noisy patch.
+    // Owner scalars in shared memory: rows 0 z_A, 1 z_B, 2 m_A, 3 m_B, 4.. c~ history ring
+    // (slot (head - q) mod (R+1) holds c~_{t-q}), A then B.
+    {
+      const float mA = own0 ? T[(HS + jy0) * TWS + HS + jx0] : 0.0f;
+      const float mB = own1 ? T[(HS + jy0) * TWS + HS + jx1] : 0.0f;
+      float zA = mA, zB = mB;
+      if (nlm_init) {
+        float ex[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+        for (int s = 0; s < 2; ++s)
 #pragma unroll
-        for (int i = 0; i < SEGL; ++i) ex[0] += wgt[s][i];
-      float o0, o1, xs[5];
-      patch_sum_reduce(wgt, ex, o0, o1, xs);
-      z0 = o0 / xs[0];
-      z1 = o1 / xs[0];
-    } else {
-      z0 = m0;
-      z1 = m1;
+          for (int i = 0; i < SEGL; ++i) ex[0] += wgt[s][i];
+        float oA, oB, xs[5];
+        patch_sum_reduce(wgt, ex, oA, oB, xs);
+        zA = own0 ? oA / xs[0] : 0.0f;
+        zB = own1 ? oB / xs[0] : 0.0f;
+      }
+      own[0 * 32] = zA;
+      own[1 * 32] = zB;
+      own[2 * 32] = mA;
+      own[3 * 32] = mB;
+#pragma unroll
+      for (int q = 1; q <= R; ++q) {
+        own[(4 + q) * 32] = 0.0f;
+        own[(4 + R + 1 + q) * 32] = 0.0f;
+      }
+      own[4 * 32] = zA - mA;  // sweep 1: c_1 = z0 (p = z0 - a), centred; head = 0
+      own[(4 + R + 1) * 32] = zB - mB;
+      if (lane <= R) nrs[lane] = 0.0f;
     }
-    if (!own1) z1 = 0.0f;
-    const float mm1 = own1 ? m1 : 0.0f;
-
-    // owner state: c~ history h[0..R] (h[0] = current), squared norms nr[0..R] (uniform)
-    float h0[R + 1], h1[R + 1], nr[R + 1];
-#pragma unroll
-    for (int q = 0; q <= R; ++q) {
-      h0[q] = 0.0f;
-      h1[q] = 0.0f;
-      nr[q] = 0.0f;
-    }
-    float G[R], Gnn, Cm;
-    // publish c~ (owners' h[0]) and the Gram row of the coming sweep
+    int head = 0;
+    float G[R], Gnn, Cm, nrR;
+    // publish c~ (owners' ring head) and the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep
     auto publish = [&]() {
+      const float* hA = own + 4 * 32;
+      const float* hB = own + (4 + R + 1) * 32;
+      const float cA = hA[head * 32], cB = hB[head * 32];
+      const float mA = own[2 * 32], mB = own[3 * 32];
       float part[R + 2];
 #pragma unroll
-      for (int q = 0; q < R; ++q) part[q] = h0[q + 1] * h0[0] + (own1 ? h1[q + 1] * h1[0] : 0.0f);
-      part[R] = h0[0] * h0[0] + (own1 ? h1[0] * h1[0] : 0.0f);
-      part[R + 1] = m0 * h0[0] + (own1 ? mm1 * h1[0] : 0.0f);
+      for (int q = 0; q < R; ++q) {
+        const int sl = (head + R - q) % (R + 1);  // c~_{t-q} relative to the new head t+1
+        part[q] = fmaf(hA[sl * 32], cA, hB[sl * 32] * cB);
+      }
+      part[R] = fmaf(cA, cA, cB * cB);
+      part[R + 1] = fmaf(mA, cA, mB * cB);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -369,131 +398,107 @@ nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, in
       for (int q = 0; q < R; ++q) G[q] = part[q];
       Gnn = part[R];
       Cm = part[R + 1];
-#pragma unroll
-      for (int q = R; q > 0; --q) nr[q] = nr[q - 1];
-      nr[0] = Gnn;
-      cb[(j0 / KS) * CB_STR + j0 % KS] = h0[0];
-      if (own1) cb[(j1 / KS) * CB_STR + j1 % KS] = h1[0];
+      if (lane == 0) nrs[head] = Gnn;
+      if (own0) cb[jy0 * CB_STR + jx0] = cA;
+      if (own1) cb[jy0 * CB_STR + jx1] = cB;
       __syncwarp();
+      nrR = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while the ring fills)
     };
-    // sweep 1: c_1 = z0 (p = z0 - a), centred
-    h0[0] = z0 - m0;
-    h1[0] = own1 ? z1 - mm1 : 0.0f;
     publish();
     tm_wait_st();
 
-    const float a0 = ref;
     int iters = P.iters;
     int fw = 0x7fffffff;  // first failure: 2 t (+1 for a non-finite norm)
     bool ovf = false;
     for (int t = 1; t <= P.iters; ++t) {
-      // (1) dot products D_k = <a_k - m, c~>
-      float Dk[2][SEGL];
+      // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
+      // (state in TMEM)
+      float u[2][SEGL];
+      float vac[R] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float usum = 0.0f;
+      bool fnorm = false, sne1 = false;
 #pragma unroll
-      for (int s = 0; s < 2; ++s)
+      for (int s = 0; s < 2; ++s) {
+        float Dk[SEGL];
 #pragma unroll
-        for (int i = 0; i < SEGL; ++i) Dk[s][i] = 0.0f;
+        for (int i = 0; i < SEGL; ++i) Dk[i] = 0.0f;
+        const float* colb = T + (s ? soff1 : soff0);
+#pragma unroll 1
+        for (int jx = 0; jx < KS; ++jx) {
+          float cvx[KS];  // column jx of c~ (broadcast loads)
 #pragma unroll
-      for (int jx = 0; jx < KS; ++jx) {
-        float cvx[KS];  // column jx of c~ (broadcast loads)
-#pragma unroll
-        for (int jy = 0; jy < KS; ++jy) cvx[jy] = cb[jy * CB_STR + jx];
-#pragma unroll
-        for (int s = 0; s < 2; ++s) {
-          const float* col = T + sgy0[s] * TWS + sgx[s] + jx;
+          for (int jy = 0; jy < KS; ++jy) cvx[jy] = cb[jy * CB_STR + jx];
+          const float* col = colb + jx;
           float v[SEGL + KS - 1];
 #pragma unroll
           for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS];
 #pragma unroll
           for (int jy = 0; jy < KS; ++jy)
 #pragma unroll
-            for (int i = 0; i < SEGL; ++i) Dk[s][i] = fmaf(v[i + jy], cvx[jy], Dk[s][i]);
+            for (int i = 0; i < SEGL; ++i) Dk[i] = fmaf(v[i + jy], cvx[jy], Dk[i]);
         }
-      }
-      // (2) per-point scalar update (state in TMEM)
-      float u[2][SEGL];
-      float vac[R] = {0.0f, 0.0f, 0.0f, 0.0f};
-      float usum = 0.0f;
-      bool fnorm = false, sne1 = false;
-      const float Gn = Gnn;
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
         float lm[8];
-        tm_ld8(t_lam(s), lm);
+        tm_ld_wait<8>(t_lam(s), lm);
 #pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
-        const int i0 = hb * 4, i1 = hb ? SEGL : 4;  // two batches of point loads (registers)
-        float st_[4][8];
-#pragma unroll
-        for (int i = i0; i < i1; ++i) tm_ld8(t_pt(s, i), st_[i - i0]);
-        tm_wait_ld(lm);
-#pragma unroll
-        for (int i = i0; i < i1; ++i) tm_tie(st_[i - i0]);
-#pragma unroll
-        for (int i = i0; i < i1; ++i) {
-          const float (&st_i)[8] = st_[i - i0];
-          const float H = st_i[0], K = st_i[1], ga = st_i[2], a2 = st_i[3];
-          const float D_ = Dk[s][i] - Cm;
-          const float X2 = fmaf(st_i[4], G[0], fmaf(st_i[5], G[1], fmaf(st_i[6], G[2], st_i[7] * G[3])));
-          const float N = (H + Gn) + 2.0f * fmaf(-(ga + 1.0f), D_, X2);
+        for (int i = 0; i < SEGL; ++i) {
+          float st[8], o[8];
+          tm_ld_wait<8>(t_pt(s, i), st);
+          const float H = st[0], K = st[1], ga = st[2], a2 = st[3];
+          const float D_ = Dk[i] - Cm;
+          const float X2 = fmaf(st[4], G[0], fmaf(st[5], G[1], fmaf(st[6], G[2], st[7] * G[3])));
+          const float N = (H + Gnn) + 2.0f * fmaf(-(ga + 1.0f), D_, X2);
           const float lam = lm[i];
           fnorm |= lam != 0.0f && !isfinite(N);
           const float Nc = fmaxf(N, 0.0f);
           const float sc = lam != 0.0f ? fminf(1.0f, lam * rsq(Nc)) : 0.0f;
           sne1 |= ((realmask >> (s * SEGL + i)) & 1u) && sc != 1.0f;
           const float B = K + D_;
-          const float ev = sc * st_i[7];
-          ovf |= ev * ev * nr[R] > kThr2 * Nc;
-          float o[8];
+          const float ev = sc * st[7];
+          ovf |= ev * ev * nrR > kThr2 * Nc;
           o[0] = fmaf(sc, fmaf(sc, Nc, -2.0f * B), a2);
           o[1] = fmaf(sc, B, -a2);
           o[2] = sc * (ga + 1.0f);
           o[3] = a2;
           o[4] = sc;
-          o[5] = sc * st_i[4];
-          o[6] = sc * st_i[5];
-          o[7] = sc * st_i[6];
+          o[5] = sc * st[4];
+          o[6] = sc * st[5];
+          o[7] = sc * st[6];
           vac[0] += o[4];
           vac[1] += o[5];
           vac[2] += o[6];
           vac[3] += o[7];
           u[s][i] = o[2];
           usum += o[2];
-          tm_st8(t_pt(s, i), o);
-        }
+          tm_st<8>(t_pt(s, i), o);
         }
       }
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
-      float ex[5] = {usum, vac[0], vac[1], vac[2], vac[3]};
-      float gA0, gA1, xs[5];
-      patch_sum_reduce(u, ex, gA0, gA1, xs);
-      // (4) consensus z' = P_C(z - g/n), c = 2 z' - z  (admm.hpp:59-65 in p-form)
-      const float U = xs[0];
-      bool zbad = false, zne = false;
+      float gA, gB, xs[5];
       {
-        const float g = fmaf(xs[1], h0[0], fmaf(xs[2], h0[1], fmaf(xs[3], h0[2], xs[4] * h0[3]))) -
-                        fmaf(-U, m0, gA0);
-        const float zn = box_clamp(fmaf(-g, inv_n, z0), P.range);
-        zbad |= !isfinite(zn);
-        zne |= zn != a0;
-        if (frames != nullptr && j0 == D / 2) frames[static_cast<int64_t>(t - 1) * plane + pix] = zn;
-        const float cn = (2.0f * zn - z0) - m0;
-#pragma unroll
-        for (int q = R; q > 0; --q) h0[q] = h0[q - 1];
-        h0[0] = cn;
-        z0 = zn;
+        const float ex[5] = {usum, vac[0], vac[1], vac[2], vac[3]};
+        patch_sum_reduce(u, ex, gA, gB, xs);
       }
-      if (own1) {
-        const float g = fmaf(xs[1], h1[0], fmaf(xs[2], h1[1], fmaf(xs[3], h1[2], xs[4] * h1[3]))) -
-                        fmaf(-U, mm1, gA1);
-        const float zn = box_clamp(fmaf(-g, inv_n, z1), P.range);
-        zbad |= !isfinite(zn);
-        zne |= zn != a0;
-        const float cn = (2.0f * zn - z1) - mm1;
+      // (4) consensus z' = P_C(z - g/n), c = 2 z' - z  (admm.hpp:59-65 in p-form);
+      // g_j = sum_q v_q c~_{t-q, j} - (sum_k ga'_k a_kj - U m_j)
+      bool zbad = false, zne = false;
+      const int nhead = (head + 1) % (R + 1);
 #pragma unroll
-        for (int q = R; q > 0; --q) h1[q] = h1[q - 1];
-        h1[0] = cn;
-        z1 = zn;
+      for (int hf = 0; hf < 2; ++hf) {
+        if (hf ? own1 : own0) {
+          float* h = own + (4 + hf * (R + 1)) * 32;
+          const float z = own[hf * 32], m = own[(2 + hf) * 32];
+          float g = 0.0f;
+#pragma unroll
+          for (int q = R - 1; q >= 0; --q) g = fmaf(xs[1 + q], h[((head + R + 1 - q) % (R + 1)) * 32], g);
+          g -= fmaf(-xs[0], m, hf ? gB : gA);
+          const float zn = box_clamp(fmaf(-g, inv_n, z), P.range);
+          zbad |= !isfinite(zn);
+          zne |= zn != a0;
+          if (hf == 0 && frames != nullptr && lane == kCenterLane)
+            frames[static_cast<int64_t>(t - 1) * plane + pix] = zn;
+          own[hf * 32] = zn;
+          h[nhead * 32] = (2.0f * zn - z) - m;
+        }
       }
       const unsigned bad_z = __ballot_sync(0xffffffffu, zbad), bad_n = __ballot_sync(0xffffffffu, fnorm);
       if (bad_z | bad_n) {
@@ -505,6 +510,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, in
         break;
       }
       if (t < P.iters) {
+        head = nhead;
         tm_wait_st();
         publish();
       }
@@ -513,18 +519,20 @@ nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, in
     const bool any_ovf = __any_sync(0xffffffffu, ovf);
     if (any_ovf) {
       // a dropped history term would have been significant: the exact p-form kernel redoes it
-      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = static_cast<int>(pix);
+      if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = pix;
     } else if (fw != 0x7fffffff) {
       if (lane == 0) {
         const int tf = fw >> 1;
         const int fail_iter = !(fw & 1) || tf == 1 ? tf : tf - 1;
-        record_failure(fail, r * cols + c, fail_iter, NLEM_FAIL_ADMM_ITERATE);
+        record_failure(fail, static_cast<int64_t>(r) * cols + c, fail_iter, NLEM_FAIL_ADMM_ITERATE);
       }
-    } else if (lane == D / 2) {
-      out[pix] = z0;
+    } else if (lane == kCenterLane) {
+      const float zc = own[0];
+      out[pix] = zc;
       if (frames)
-        for (int t = iters; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = z0;
+        for (int t = iters; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = zc;
     }
+    __syncwarp();
     pix = nxt;
     buf ^= 1;
   }
@@ -534,7 +542,10 @@ nlem_pixels_lr(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, in
 }
 
 bool nlem_lr_supported(const NlemLaunch& L) {
-  return L.P.solver == NLEM_SOLVER_ADMM && L.P.patch == KS && L.P.search == SW;
+  // 32-bit pixel indexing inside the kernel
+  const int64_t lim = int64_t(1) << 30;
+  return L.P.solver == NLEM_SOLVER_ADMM && L.P.patch == KS && L.P.search == SW &&
+         L.out_rows * L.cols < lim && L.rows < lim && L.pad_cols < lim;
 }
 
 cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
@@ -547,7 +558,8 @@ cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, i
   int64_t grid = device_caps().sms;
   grid = std::max<int64_t>(1, std::min<int64_t>(grid, (pixels + WARPS - 1) / WARPS));
   kfn<<<static_cast<unsigned>(grid), WARPS * 32, SMEM_BYTES, stream>>>(
-      L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out, L.frames, counter,
+      L.pad, static_cast<int>(L.pad_cols), static_cast<int>(L.rows), static_cast<int>(L.cols),
+      static_cast<int>(L.out_row0), static_cast<int>(pixels), L.P, L.out, L.frames, counter,
       ovf_list, ovf_count, L.fail);
   return cudaGetLastError();
 }

@@ -1,0 +1,6 @@
+cd $GRAFT_REPO_ROOT
+NLEM_KERNEL=lr timeout 300 python tools/dev/lr_iters.py
+timeout 300 python tools/prof_nlem.py --what nlem > /dev/null 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:nlem_pixels_lr -s 1 -c 1 -f \
+  -o gpurun_out/prof_lr python tools/prof_nlem.py --what nlem > gpurun_out/ncu_lr.log 2>&1
+tail -2 gpurun_out/ncu_lr.log
