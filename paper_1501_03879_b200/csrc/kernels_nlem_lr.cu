@@ -45,27 +45,26 @@ namespace nlemk {
 
 namespace lr {
 
-constexpr int KS = 7, SW = 21, D = KS * KS, HS = SW / 2;
+constexpr int KS = 7, SW = 21, HS = SW / 2;
 constexpr int TH = SW + KS - 1;  // 27
 constexpr int TWS = 35;          // tile row stride (bank-distinct segment starts)
 constexpr int TILE = (TH * TWS + 3) / 4 * 4;  // floats per tile buffer (16-byte multiple)
-constexpr int WARPS = 16;
+#ifndef NLEM_LR_WARPS
+#define NLEM_LR_WARPS 16
+#endif
+constexpr int WARPS = NLEM_LR_WARPS;  // pixel-warps per CTA (1 CTA per SM)
 constexpr int SEGL = 7;  // points per segment
 constexpr int R = 4;     // history ring
 constexpr int NF = 8;    // state fields per point in TMEM
-#ifndef NLEM_LR_NPB
-#define NLEM_LR_NPB 1
-#endif
-constexpr int NPB = NLEM_LR_NPB;  // points per TMEM load/store in the scalar phase
 constexpr int RED_STR = 36;
 constexpr int CB_STR = 8;
 // per-warp shared memory (floats)
-constexpr int W_TILE0 = 0;
 constexpr int W_RED = 2 * TILE;
 constexpr int W_CB = W_RED + 32 * RED_STR;
-constexpr int W_OWN = W_CB + KS * CB_STR;         // [4 + 2 (R+1)][32] owner scalars
+constexpr int W_OWN = W_CB + KS * CB_STR;        // [4 + 2 (R+1)][32] owner scalars
 constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 ring
-constexpr int W_TOTAL = W_NR + 8;
+constexpr int W_GR = W_NR + 8;  // [8] Gram row of the coming sweep: G[0..R-1], ||c~||^2, <m, c~>, ||c~_{t+1-R}||^2
+constexpr int W_TOTAL = W_GR + 8;
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
 constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
 constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2
@@ -137,6 +136,16 @@ __device__ __forceinline__ void tm_st<16>(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[15]))
       : "memory");
 }
+
+__device__ __forceinline__ void tm_st1(uint32_t taddr, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(__float_as_uint(v)) : "memory");
+}
+__device__ __forceinline__ void tm_st2(uint32_t taddr, float a, float b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(__float_as_uint(a)), "r"(__float_as_uint(b)) : "memory");
+}
+__device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d)) : "memory");
+}
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float box_clamp(float v, const nlem_box& box) {
@@ -158,6 +167,14 @@ __device__ __forceinline__ void seg_of(int lane, int slot, int& gx, int& gy0, bo
     else if (lane < 31) { gx = lane - 10; gy0 = 14; }
     else { gx = 0; gy0 = 14; valid = false; }
   }
+}
+
+// Forces a float2 into one aligned 64-bit register pair (the FFMA2 operand form), so the
+// compiler does not re-pair two scattered 32-bit registers with MOVs at every use.
+__device__ __forceinline__ float2 pin_pair(float2 v) {
+  unsigned long long b = (static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
+  asm volatile("" : "+l"(b));
+  return make_float2(__uint_as_float(static_cast<unsigned>(b)), __uint_as_float(static_cast<unsigned>(b >> 32)));
 }
 
 // sum of red[row][0..31] (row stride RED_STR, 16-byte aligned) in a fixed tree order
@@ -185,6 +202,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   float* const W = smem + warp * W_TOTAL;
   float* const red = W + W_RED;
   float* const cb = W + W_CB;
+  float* const gram = W + W_GR;
   float* const own = W + W_OWN + lane;  // owner scalars, row stride 32 (lane-private column)
   float* const nrs = W + W_NR;          // ||c~||^2 history ring (warp-uniform)
 
@@ -200,8 +218,15 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const uint32_t tbase = *tm_base_slot;
   const uint32_t tw = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
                       static_cast<uint32_t>((warp >> 2) * 128);
-  auto t_pt = [&](int slot, int i) { return tw + static_cast<uint32_t>((slot * SEGL + i) * NF); };
-  auto t_lam = [&](int slot) { return tw + static_cast<uint32_t>(112 + slot * 8); };
+  // TMEM addresses are formed right before each access (opaque to CSE/hoisting): kept as
+  // long-lived uniform registers they exhaust the uniform register file and spill
+  auto t_at = [&](uint32_t col) {
+    uint32_t a;
+    asm volatile("add.u32 %0, %1, %2;" : "=r"(a) : "r"(tw), "r"(col));
+    return a;
+  };
+  auto t_pt = [&](int slot, int i) { return t_at(static_cast<uint32_t>((slot * SEGL + i) * NF)); };
+  auto t_lam = [&](int slot) { return t_at(static_cast<uint32_t>(112 + slot * 8)); };
 
   // lane geometry: segment column offsets in the tile
   int sgx0, sgy00, sgx1, sgy01;
@@ -259,71 +284,78 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 
     // ---- distances ||a_k - a_self||^2 (patch.cpp:52-61), weights, lambdas; state init
     unsigned realmask = 0;  // bit s*7+i: grid point inside the clipped window (patch.cpp:72-76)
-    float wgt[2][SEGL];
+    float2 wgt[SEGL];  // (slot 0, slot 1) pairs
+    {
+      // the two slots of a lane run as the two halves of FADD2 / FFMA2 pairs
+      float2 A2[SEGL];
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      float A2[SEGL];
-#pragma unroll
-      for (int i = 0; i < SEGL; ++i) A2[i] = 0.0f;
-      const float* col = T + (s ? soff1 : soff0);
+      for (int i = 0; i < SEGL; ++i) A2[i] = make_float2(0.0f, 0.0f);
 #pragma unroll 1
       for (int jx = 0; jx < KS; ++jx) {
-        float v[SEGL + KS - 1], ac[KS];
+        float2 v[SEGL + KS - 1];
 #pragma unroll
-        for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS + jx];
+        for (int e = 0; e < SEGL + KS - 1; ++e)
+          v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
 #pragma unroll
-        for (int jy = 0; jy < KS; ++jy) ac[jy] = T[(HS + jy) * TWS + HS + jx];
-#pragma unroll
-        for (int jy = 0; jy < KS; ++jy)
+        for (int jy = 0; jy < KS; ++jy) {
+          const float ac = -T[(HS + jy) * TWS + HS + jx];
+          const float2 nac = make_float2(ac, ac);
 #pragma unroll
           for (int i = 0; i < SEGL; ++i) {
-            const float df = v[i + jy] - ac[jy];
-            A2[i] = fmaf(df, df, A2[i]);
+            const float2 df = __fadd2_rn(v[i + jy], nac);
+            A2[i] = __ffma2_rn(df, df, A2[i]);
           }
+        }
       }
-      const int gx = s ? sgx1 : sgx0, gy0 = s ? sgy01 : sgy00;
-      const bool colreal = (s ? sval1 : sval0) && gx >= gc0 && gx <= gc1;
-      float lm[8];
 #pragma unroll
-      for (int i = 0; i < SEGL; ++i) {
-        const bool real = colreal && gy0 + i >= gr0 && gy0 + i <= gr1;
-        wgt[s][i] = real ? expf(-A2[i] * P.inv_h2) : 0.0f;
-        realmask |= real ? 1u << (s * SEGL + i) : 0u;
-        lm[i] = inv_mu * wgt[s][i];
-        // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0
-        const float st[8] = {A2[i], -A2[i], 0.0f, A2[i], 0.0f, 0.0f, 0.0f, 0.0f};
-        tm_st<8>(t_pt(s, i), st);
+      for (int s = 0; s < 2; ++s) {
+        const int gx = s ? sgx1 : sgx0, gy0 = s ? sgy01 : sgy00;
+        const bool colreal = (s ? sval1 : sval0) && gx >= gc0 && gx <= gc1;
+        float lm[8];
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) {
+          const float a2 = s ? A2[i].y : A2[i].x;
+          const bool real = colreal && gy0 + i >= gr0 && gy0 + i <= gr1;
+          const float w = real ? expf(-a2 * P.inv_h2) : 0.0f;
+          if (s) wgt[i].y = w; else wgt[i].x = w;
+          realmask |= real ? 1u << (s * SEGL + i) : 0u;
+          lm[i] = inv_mu * (s ? wgt[i].y : wgt[i].x);
+          // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0
+          const float st[8] = {a2, -a2, 0.0f, a2, 0.0f, 0.0f, 0.0f, 0.0f};
+          tm_st<8>(t_pt(s, i), st);
+        }
+        lm[7] = 0.0f;
+        tm_st<8>(t_lam(s), lm);
       }
-      lm[7] = 0.0f;
-      tm_st<8>(t_lam(s), lm);
     }
 
     // ---- patch-sum pass (sum_k u_k a_k per coordinate) + transpose reduction to the owners.
     // Half A rows (jx - 0) * 7 + jy, half B rows (jx - 4) * 7 + jy, then 5 extra scalars.
-    auto patch_sum_reduce = [&](const float (&u)[2][SEGL], const float (&extra)[5], float& oA,
+    auto patch_sum_reduce = [&](const float2 (&u2)[SEGL], const float (&extra)[5], float& oA,
                                 float& oB, float (&xs)[5]) {
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int jxa = hf ? 4 : 0, jxb = hf ? KS : 4;
 #pragma unroll 1
         for (int jx = jxa; jx < jxb; ++jx) {
-          float gc[KS];
+          // keep the (slot 0, slot 1) weights in aligned 64-bit register pairs for FFMA2
+          float2 up[SEGL];
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy) gc[jy] = 0.0f;
+          for (int i = 0; i < SEGL; ++i) up[i] = pin_pair(u2[i]);
+          float2 gc[KS];
 #pragma unroll
-          for (int s = 0; s < 2; ++s) {
-            const float* col = T + (s ? soff1 : soff0) + jx;
-            float v[SEGL + KS - 1];
+          for (int jy = 0; jy < KS; ++jy) gc[jy] = make_float2(0.0f, 0.0f);
+          float2 v[SEGL + KS - 1];
 #pragma unroll
-            for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS];
+          for (int e = 0; e < SEGL + KS - 1; ++e)
+            v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
 #pragma unroll
-            for (int jy = 0; jy < KS; ++jy)
+          for (int jy = 0; jy < KS; ++jy)
 #pragma unroll
-              for (int i = 0; i < SEGL; ++i) gc[jy] = fmaf(u[s][i], v[i + jy], gc[jy]);
-          }
+            for (int i = 0; i < SEGL; ++i) gc[jy] = __ffma2_rn(up[i], v[i + jy], gc[jy]);
           float* rrow = red + (jx - jxa) * KS * RED_STR + lane;
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = gc[jy];
+          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = gc[jy].x + gc[jy].y;
         }
         if (hf) {
 #pragma unroll
@@ -355,7 +387,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
-          for (int i = 0; i < SEGL; ++i) ex[0] += wgt[s][i];
+          for (int i = 0; i < SEGL; ++i) ex[0] += (s ? wgt[i].y : wgt[i].x);
         float oA, oB, xs[5];
         patch_sum_reduce(wgt, ex, oA, oB, xs);
         zA = own0 ? oA / xs[0] : 0.0f;
@@ -375,7 +407,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       if (lane <= R) nrs[lane] = 0.0f;
     }
     int head = 0;
-    float G[R], Gnn, Cm, nrR;
     // publish c~ (owners' ring head) and the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep
     auto publish = [&]() {
       const float* hA = own + 4 * 32;
@@ -395,14 +426,13 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
         for (int q = 0; q < R + 2; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
 #pragma unroll
-      for (int q = 0; q < R; ++q) G[q] = part[q];
-      Gnn = part[R];
-      Cm = part[R + 1];
-      if (lane == 0) nrs[head] = Gnn;
+      for (int q = 0; q < R + 2; ++q) gram[q] = part[q];  // same value in every lane
+      if (lane == 0) nrs[head] = part[R];
       if (own0) cb[jy0 * CB_STR + jx0] = cA;
       if (own1) cb[jy0 * CB_STR + jx1] = cB;
       __syncwarp();
-      nrR = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while the ring fills)
+      if (lane == 0) gram[R + 2] = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while filling)
+      __syncwarp();
     };
     publish();
     tm_wait_st();
@@ -413,32 +443,38 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     for (int t = 1; t <= P.iters; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
-      float u[2][SEGL];
+      float2 u[SEGL];  // ga' of (slot 0, slot 1): the FFMA2 pairs of the patch-sum pass
       float vac[R] = {0.0f, 0.0f, 0.0f, 0.0f};
       float usum = 0.0f;
       bool fnorm = false, sne1 = false;
+      float2 Dk2[SEGL];
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+      for (int jx = 0; jx < KS; ++jx) {
+        float cvx[KS];  // column jx of c~ (broadcast loads; FFMA2 takes it as a scalar operand)
+#pragma unroll
+        for (int jy = 0; jy < KS; ++jy) cvx[jy] = cb[jy * CB_STR + jx];
+        float2 v[SEGL + KS - 1];  // (slot 0, slot 1) tile values
+#pragma unroll
+        for (int e = 0; e < SEGL + KS - 1; ++e)
+          v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
+#pragma unroll
+        for (int jy = 0; jy < KS; ++jy)
+#pragma unroll
+          for (int i = 0; i < SEGL; ++i) Dk2[i] = __ffma2_rn(v[i + jy], make_float2(cvx[jy], cvx[jy]), Dk2[i]);
+      }
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         float Dk[SEGL];
 #pragma unroll
-        for (int i = 0; i < SEGL; ++i) Dk[i] = 0.0f;
-        const float* colb = T + (s ? soff1 : soff0);
-#pragma unroll 1
-        for (int jx = 0; jx < KS; ++jx) {
-          float cvx[KS];  // column jx of c~ (broadcast loads)
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy) cvx[jy] = cb[jy * CB_STR + jx];
-          const float* col = colb + jx;
-          float v[SEGL + KS - 1];
-#pragma unroll
-          for (int e = 0; e < SEGL + KS - 1; ++e) v[e] = col[e * TWS];
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy)
-#pragma unroll
-            for (int i = 0; i < SEGL; ++i) Dk[i] = fmaf(v[i + jy], cvx[jy], Dk[i]);
-        }
+        for (int i = 0; i < SEGL; ++i) Dk[i] = s ? Dk2[i].y : Dk2[i].x;
         float lm[8];
         tm_ld_wait<8>(t_lam(s), lm);
+        float G[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) G[q] = gram[q];
+        const float Gnn = gram[R], Cm = gram[R + 1], nrR = gram[R + 2];
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
           float st[8], o[8];
@@ -467,9 +503,14 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           vac[1] += o[5];
           vac[2] += o[6];
           vac[3] += o[7];
-          u[s][i] = o[2];
+          if (s) u[i].y = o[2]; else u[i].x = o[2];
           usum += o[2];
-          tm_st<8>(t_pt(s, i), o);
+          {
+            // one column per store: x8 register tuples fragment the register file (spills)
+            const uint32_t ta = t_pt(s, i);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) tm_st1(ta + q, o[q]);
+          }
         }
       }
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
