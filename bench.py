@@ -373,7 +373,7 @@ def main():
                 "h2d_bytes_per_step": int(band_in.nbytes), "d2h_bytes_per_step": int(nrows * cols * 4),
                 "entry": "nlem_denoise_rows_host (C-ABI, pinned host buffers)"},
         "clocks": clk,
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # pad + low-rank pixel kernel + tile kernel over its hand-off list
         "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
         "secondary": secondary,
         "step_ms": [round(x, 2) for x in step_ms],
