@@ -462,6 +462,14 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
       if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int), s);
       if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 2, scratch + 1, scratch, s);
       if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 2, scratch + 1, s);
+      static const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;
+      if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
+        int handed = 0;
+        e = cudaMemcpyAsync(&handed, scratch + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        std::fprintf(stderr, "nlem_lr: %lld pixels, %d handed to the tile kernel\n",
+                     static_cast<long long>(pixels), handed);
+      }
       if (scratch) {
         const cudaError_t ef = cudaFreeAsync(scratch, s);
         if (e == cudaSuccess) e = ef;

@@ -352,3 +352,85 @@ def test_tile_kernel_admm_failure_reports_pixel_and_iteration(nb):
     with pytest.raises(nb.NumericFailure) as e2:
         nb.nlem_denoise(img, p)
     assert str(e2.value) == msg
+
+
+# ---------------------------------------------------------------- low-rank kernel specifics
+_TILE_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, %(root)r)
+import paper_1501_03879_b200 as nb
+a = np.load(%(inp)r)
+kw = %(kw)r
+box = nb.BoxConstraint.unconstrained() if kw.pop("unbounded", False) else nb.BoxConstraint.interval(0.0, 255.0)
+p = nb.NlemParams(**kw, range=box)
+try:
+    out = nb.nlem_denoise_snapshots(a, p)
+    np.save(%(out)r, out)
+except nb.NumericFailure as e:
+    open(%(out)r + ".txt", "w").write(str(e))
+"""
+
+
+def _run_forced_kernel(kernel, img, kw, tmp_path, stats=None):
+    """nlem_denoise_snapshots in a child process with NLEM_KERNEL=<kernel> (the choice is read
+    once per process).  stats: a list that receives the low-rank kernel's hand-off lines."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    inp, out = str(tmp_path / "in.npy"), str(tmp_path / f"out_{kernel}.npy")
+    np.save(inp, img)
+    env = dict(os.environ, NLEM_KERNEL=kernel)
+    if stats is not None:
+        env["NLEM_LR_STATS"] = "1"
+    r = subprocess.run([sys.executable, "-c", _TILE_CHILD % dict(root=root, inp=inp, out=out, kw=kw)],
+                       env=env, check=True, timeout=600, capture_output=True, text=True)
+    if stats is not None:
+        stats.extend(l for l in r.stderr.splitlines() if l.startswith("nlem_lr:"))
+    if os.path.exists(out + ".txt"):
+        return open(out + ".txt").read()
+    return np.load(out)
+
+
+def test_lr_ring_handoff_small_mu(nb, oracle, tmp_path):
+    """mu = 1e-3 (the reference default, types.hpp:121): lambda = w/mu ~ 1000 makes s_k = 1 for
+    most points, so the low-rank kernel's history ring cannot drop terms and hands the pixels to
+    the exact p-form tile kernel through its device-side list.  Frames and output vs oracle."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(36, 36, 5, 3, 20.0)
+    for init in ("nlm", "noisy"):
+        g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(20.0, 49), iters=8,
+                            mu=1e-3, init=init)
+        fg = nb.nlem_denoise_snapshots(noisy, g)
+        _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
+        assert np.abs(fg - fo).max() <= TOL
+    # the hand-off path really ran (and the config-like mu = 1 case hands nothing off)
+    for mu, expect_handoff in ((1e-3, True), (1.0, False)):
+        stats = []
+        kw = dict(search=21, patch=7, h=synth.reference_h(20.0, 49), solver="admm",
+                  solver_iters=8, mu=mu, init_mode="nlm")
+        _run_forced_kernel("lr", noisy, kw, tmp_path, stats)
+        handed = [int(l.split(",")[1].split()[0]) for l in stats]
+        assert handed, stats
+        assert (sum(handed) > 0) == expect_handoff, stats
+
+
+def test_lr_kernel_matches_tile_kernel(nb, tmp_path):
+    """The low-rank kernel (default for k=7/S=21 ADMM) and the exact p-form tile kernel agree
+    on every frame of a config-3-parameter crop to FP32 rounding, and report the same
+    NumericFailure (pixel and iteration) on an overflowing input."""
+    from paper_1501_03879_b200 import synth
+
+    _, noisy = synth.noisy_image(56, 64, 12, 8, 30.0)
+    kw = dict(search=21, patch=7, h=synth.reference_h(30.0, 49), solver="admm", solver_iters=12,
+              mu=1.0, init_mode="nlm")
+    lr = _run_forced_kernel("lr", noisy, kw, tmp_path)
+    tile = _run_forced_kernel("tile", noisy, kw, tmp_path)
+    assert np.abs(lr - tile).max() <= 2e-3
+    img = np.zeros((30, 30), np.float32)
+    img[12:18, 12:18] = np.where(np.add.outer(np.arange(6), np.arange(6)) % 2 == 0, 0.0, 3e19)
+    kw = dict(search=21, patch=7, h=1e30, sigma=10.0, solver="admm", solver_iters=4, mu=1.0,
+              unbounded=True)
+    assert _run_forced_kernel("lr", img, kw, tmp_path) == _run_forced_kernel("tile", img, kw, tmp_path)
