@@ -225,8 +225,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     asm volatile("add.u32 %0, %1, %2;" : "=r"(a) : "r"(tw), "r"(col));
     return a;
   };
-  auto t_pt = [&](int slot, int i) { return t_at(static_cast<uint32_t>((slot * SEGL + i) * NF)); };
-  auto t_lam = [&](int slot) { return t_at(static_cast<uint32_t>(112 + slot * 8)); };
+  // column layout per lane: point pair i (slot 0 and slot 1 point i) = 16 columns, field q of
+  // slot s at 2 q + s, so one x16 load yields 8 (slot 0, slot 1) register pairs for the paired
+  // (FFMA2 / FMUL2 / FADD2) scalar update; lambdas of the 14 points at 112 + 2 i + s
+  auto t_pt = [&](int i) { return t_at(static_cast<uint32_t>(i * 2 * NF)); };
+  auto t_lam = [&]() { return t_at(static_cast<uint32_t>(2 * NF * SEGL)); };
 
   // lane geometry: segment column offsets in the tile
   int sgx0, sgy00, sgx1, sgy01;
@@ -307,11 +310,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           }
         }
       }
+      float lm[16];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
         const int gx = s ? sgx1 : sgx0, gy0 = s ? sgy01 : sgy00;
         const bool colreal = (s ? sval1 : sval0) && gx >= gc0 && gx <= gc1;
-        float lm[8];
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
           const float a2 = s ? A2[i].y : A2[i].x;
@@ -319,14 +322,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           const float w = real ? expf(-a2 * P.inv_h2) : 0.0f;
           if (s) wgt[i].y = w; else wgt[i].x = w;
           realmask |= real ? 1u << (s * SEGL + i) : 0u;
-          lm[i] = inv_mu * (s ? wgt[i].y : wgt[i].x);
-          // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0
-          const float st[8] = {a2, -a2, 0.0f, a2, 0.0f, 0.0f, 0.0f, 0.0f};
-          tm_st<8>(t_pt(s, i), st);
+          lm[2 * i + s] = inv_mu * w;
         }
-        lm[7] = 0.0f;
-        tm_st<8>(t_lam(s), lm);
       }
+      lm[14] = lm[15] = 0.0f;
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) {
+        // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0 (slot-interleaved)
+        const float st[16] = {A2[i].x, A2[i].y, -A2[i].x, -A2[i].y, 0.0f, 0.0f, A2[i].x, A2[i].y,
+                              0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+        tm_st<16>(t_pt(i), st);
+      }
+      tm_st<16>(t_lam(), lm);
     }
 
     // ---- patch-sum pass (sum_k u_k a_k per coordinate) + transpose reduction to the owners.
@@ -464,54 +471,72 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
           for (int i = 0; i < SEGL; ++i) Dk2[i] = __ffma2_rn(v[i + jy], make_float2(cvx[jy], cvx[jy]), Dk2[i]);
       }
-#pragma unroll
-      for (int s = 0; s < 2; ++s) {
-        float Dk[SEGL];
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) Dk[i] = s ? Dk2[i].y : Dk2[i].x;
-        float lm[8];
-        tm_ld_wait<8>(t_lam(s), lm);
+      {
+        float lm[16];
+        tm_ld_wait<16>(t_lam(), lm);
         float G[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) G[q] = gram[q];
         const float Gnn = gram[R], Cm = gram[R + 1], nrR = gram[R + 2];
+        float2 vac2[R];
+#pragma unroll
+        for (int q = 0; q < R; ++q) vac2[q] = make_float2(0.0f, 0.0f);
+        float2 us2 = make_float2(0.0f, 0.0f);
+        const float2 one2 = make_float2(1.0f, 1.0f);
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
-          float st[8], o[8];
-          tm_ld_wait<8>(t_pt(s, i), st);
-          const float H = st[0], K = st[1], ga = st[2], a2 = st[3];
-          const float D_ = Dk[i] - Cm;
-          const float X2 = fmaf(st[4], G[0], fmaf(st[5], G[1], fmaf(st[6], G[2], st[7] * G[3])));
-          const float N = (H + Gnn) + 2.0f * fmaf(-(ga + 1.0f), D_, X2);
-          const float lam = lm[i];
-          fnorm |= lam != 0.0f && !isfinite(N);
-          const float Nc = fmaxf(N, 0.0f);
-          const float sc = lam != 0.0f ? fminf(1.0f, lam * rsq(Nc)) : 0.0f;
-          sne1 |= ((realmask >> (s * SEGL + i)) & 1u) && sc != 1.0f;
-          const float B = K + D_;
-          const float ev = sc * st[7];
-          ovf |= ev * ev * nrR > kThr2 * Nc;
-          o[0] = fmaf(sc, fmaf(sc, Nc, -2.0f * B), a2);
-          o[1] = fmaf(sc, B, -a2);
-          o[2] = sc * (ga + 1.0f);
-          o[3] = a2;
-          o[4] = sc;
-          o[5] = sc * st[4];
-          o[6] = sc * st[5];
-          o[7] = sc * st[6];
-          vac[0] += o[4];
-          vac[1] += o[5];
-          vac[2] += o[6];
-          vac[3] += o[7];
-          if (s) u[i].y = o[2]; else u[i].x = o[2];
-          usum += o[2];
+          // point i of both slots as one register pair per field
+          float st[16];
+          tm_ld_wait<16>(t_pt(i), st);
+          const float2 H = make_float2(st[0], st[1]), K = make_float2(st[2], st[3]);
+          const float2 ga = make_float2(st[4], st[5]), a2 = make_float2(st[6], st[7]);
+          const float2 al0 = make_float2(st[8], st[9]), al1 = make_float2(st[10], st[11]);
+          const float2 al2 = make_float2(st[12], st[13]), al3 = make_float2(st[14], st[15]);
+          const float2 D_ = __fadd2_rn(Dk2[i], make_float2(-Cm, -Cm));
+          const float2 X2 = __ffma2_rn(al0, make_float2(G[0], G[0]),
+                            __ffma2_rn(al1, make_float2(G[1], G[1]),
+                            __ffma2_rn(al2, make_float2(G[2], G[2]), __fmul2_rn(al3, make_float2(G[3], G[3])))));
+          const float2 gp1 = __fadd2_rn(ga, one2);
+          const float2 t2 = __ffma2_rn(make_float2(-gp1.x, -gp1.y), D_, X2);
+          const float2 N = __ffma2_rn(make_float2(2.0f, 2.0f), t2, __fadd2_rn(H, make_float2(Gnn, Gnn)));
+          float2 sc, Nc;
           {
-            // one column per store: x8 register tuples fragment the register file (spills)
-            const uint32_t ta = t_pt(s, i);
+            const float lx = lm[2 * i], ly = lm[2 * i + 1];
+            fnorm |= (lx != 0.0f && !isfinite(N.x)) || (ly != 0.0f && !isfinite(N.y));
+            Nc = make_float2(fmaxf(N.x, 0.0f), fmaxf(N.y, 0.0f));
+            sc.x = lx != 0.0f ? fminf(1.0f, lx * rsq(Nc.x)) : 0.0f;
+            sc.y = ly != 0.0f ? fminf(1.0f, ly * rsq(Nc.y)) : 0.0f;
+            sne1 |= (((realmask >> i) & 1u) && sc.x != 1.0f) ||
+                    (((realmask >> (SEGL + i)) & 1u) && sc.y != 1.0f);
+          }
+          const float2 B = __fadd2_rn(K, D_);
+          const float2 ev = __fmul2_rn(sc, al3);
+          const float2 evv = __fmul2_rn(__fmul2_rn(ev, ev), make_float2(nrR, nrR));
+          ovf |= evv.x > kThr2 * Nc.x || evv.y > kThr2 * Nc.y;
+          float o[16];
+          const float2 oH = __ffma2_rn(sc, __ffma2_rn(sc, Nc, __fmul2_rn(make_float2(-2.0f, -2.0f), B)), a2);
+          const float2 oK = __ffma2_rn(sc, B, make_float2(-a2.x, -a2.y));
+          const float2 oga = __fmul2_rn(sc, gp1);
+          const float2 o1 = __fmul2_rn(sc, al0), o2 = __fmul2_rn(sc, al1), o3 = __fmul2_rn(sc, al2);
+          o[0] = oH.x; o[1] = oH.y; o[2] = oK.x; o[3] = oK.y; o[4] = oga.x; o[5] = oga.y;
+          o[6] = a2.x; o[7] = a2.y; o[8] = sc.x; o[9] = sc.y; o[10] = o1.x; o[11] = o1.y;
+          o[12] = o2.x; o[13] = o2.y; o[14] = o3.x; o[15] = o3.y;
+          vac2[0] = __fadd2_rn(vac2[0], sc);
+          vac2[1] = __fadd2_rn(vac2[1], o1);
+          vac2[2] = __fadd2_rn(vac2[2], o2);
+          vac2[3] = __fadd2_rn(vac2[3], o3);
+          u[i] = oga;
+          us2 = __fadd2_rn(us2, oga);
+          {
+            // one column per store: register tuples fragment the register file (spills)
+            const uint32_t ta = t_pt(i);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) tm_st1(ta + q, o[q]);
+            for (int q = 0; q < 16; ++q) tm_st1(ta + q, o[q]);
           }
         }
+#pragma unroll
+        for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
+        usum = us2.x + us2.y;
       }
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
       float gA, gB, xs[5];
