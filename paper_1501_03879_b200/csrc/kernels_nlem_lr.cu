@@ -38,6 +38,7 @@
 //    Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce.
 #include <algorithm>
 #include <cstdlib>
+#include <utility>
 
 #include "launch.h"
 
@@ -146,6 +147,34 @@ __device__ __forceinline__ void tm_st2(uint32_t taddr, float a, float b) {
 __device__ __forceinline__ void tm_st4(uint32_t taddr, float a, float b, float c, float d) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)), "r"(__float_as_uint(d)) : "memory");
 }
+// Base + compile-time column offset (PTX [taddr+imm]): one long-lived base register instead of
+// one uniform register per address (those exhausted the uniform register file) or a per-access
+// add + R2UR.
+template <int OFF>
+__device__ __forceinline__ void tm_st1c(uint32_t base, float v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0+%1], {%2};" ::"r"(base), "n"(OFF),
+               "r"(__float_as_uint(v))
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tm_ld16c_wait(uint32_t base, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16+%17];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(base), "n"(OFF)
+      : "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  [&]<int... I>(std::integer_sequence<int, I...>) { (f(std::integral_constant<int, I>{}), ...); }(
+      std::make_integer_sequence<int, N>{});
+}
+
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ float box_clamp(float v, const nlem_box& box) {
@@ -197,7 +226,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
                int plane, NlemDevParams P, float* out, float* frames, int* work_counter,
                int* ovf_list, int* ovf_count, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index through a shuffle: the compiler then knows it is warp-uniform (uniform datapath)
+  const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
+  const int lane = threadIdx.x & 31;
   uint32_t* tm_base_slot = reinterpret_cast<uint32_t*>(smem + WARPS * W_TOTAL);
   float* const W = smem + warp * W_TOTAL;
   float* const red = W + W_RED;
@@ -220,11 +251,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
                       static_cast<uint32_t>((warp >> 2) * 128);
   // TMEM addresses are formed right before each access (opaque to CSE/hoisting): kept as
   // long-lived uniform registers they exhaust the uniform register file and spill
-  auto t_at = [&](uint32_t col) {
-    uint32_t a;
-    asm volatile("add.u32 %0, %1, %2;" : "=r"(a) : "r"(tw), "r"(col));
-    return a;
-  };
+  auto t_at = [&](uint32_t col) { return tw + col; };
   // column layout per lane: point pair i (slot 0 and slot 1 point i) = 16 columns, field q of
   // slot s at 2 q + s, so one x16 load yields 8 (slot 0, slot 1) register pairs for the paired
   // (FFMA2 / FMUL2 / FADD2) scalar update; lambdas of the 14 points at 112 + 2 i + s
@@ -473,7 +500,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       }
       {
         float lm[16];
-        tm_ld_wait<16>(t_lam(), lm);
+        tm_ld16c_wait<2 * NF * SEGL>(tw, lm);
         float G[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) G[q] = gram[q];
@@ -483,11 +510,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         for (int q = 0; q < R; ++q) vac2[q] = make_float2(0.0f, 0.0f);
         float2 us2 = make_float2(0.0f, 0.0f);
         const float2 one2 = make_float2(1.0f, 1.0f);
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) {
+        static_for<SEGL>([&](auto ic) {
+          constexpr int i = decltype(ic)::value;
           // point i of both slots as one register pair per field
           float st[16];
-          tm_ld_wait<16>(t_pt(i), st);
+          tm_ld16c_wait<i * 2 * NF>(tw, st);
           const float2 H = make_float2(st[0], st[1]), K = make_float2(st[2], st[3]);
           const float2 ga = make_float2(st[4], st[5]), a2 = make_float2(st[6], st[7]);
           const float2 al0 = make_float2(st[8], st[9]), al1 = make_float2(st[10], st[11]);
@@ -527,13 +554,12 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           vac2[3] = __fadd2_rn(vac2[3], o3);
           u[i] = oga;
           us2 = __fadd2_rn(us2, oga);
-          {
-            // one column per store: register tuples fragment the register file (spills)
-            const uint32_t ta = t_pt(i);
-#pragma unroll
-            for (int q = 0; q < 16; ++q) tm_st1(ta + q, o[q]);
-          }
-        }
+          // one column per store: register tuples fragment the register file (spills)
+          static_for<16>([&](auto qc) {
+            constexpr int q = decltype(qc)::value;
+            tm_st1c<i * 2 * NF + q>(tw, o[q]);
+          });
+        });
 #pragma unroll
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
         usum = us2.x + us2.y;
