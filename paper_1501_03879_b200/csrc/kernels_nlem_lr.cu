@@ -57,6 +57,9 @@ constexpr int WARPS = NLEM_LR_WARPS;  // pixel-warps per CTA (1 CTA per SM)
 constexpr int SEGL = 7;  // points per segment
 constexpr int R = 4;     // history ring
 constexpr int NF = 8;    // state fields per point in TMEM
+#ifndef NLEM_LR_ST
+#define NLEM_LR_ST 2  // columns per tcgen05.st in the sweep (1, 2 or 4)
+#endif
 constexpr int RED_STR = 36;
 constexpr int CB_STR = 8;
 // per-warp shared memory (floats)
@@ -154,6 +157,19 @@ template <int OFF>
 __device__ __forceinline__ void tm_st1c(uint32_t base, float v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0+%1], {%2};" ::"r"(base), "n"(OFF),
                "r"(__float_as_uint(v))
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tm_st2c(uint32_t base, float a, float b) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0+%1], {%2, %3};" ::"r"(base), "n"(OFF),
+               "r"(__float_as_uint(a)), "r"(__float_as_uint(b))
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tm_st4c(uint32_t base, float a, float b, float c, float d) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0+%1], {%2, %3, %4, %5};" ::"r"(base), "n"(OFF),
+               "r"(__float_as_uint(a)), "r"(__float_as_uint(b)), "r"(__float_as_uint(c)),
+               "r"(__float_as_uint(d))
                : "memory");
 }
 template <int OFF>
@@ -554,11 +570,23 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           vac2[3] = __fadd2_rn(vac2[3], o3);
           u[i] = oga;
           us2 = __fadd2_rn(us2, oga);
-          // one column per store: register tuples fragment the register file (spills)
+          // column pairs per store (x8 / x16 register tuples fragment the register file: spills)
+#if NLEM_LR_ST == 4
+          static_for<4>([&](auto qc) {
+            constexpr int q = decltype(qc)::value;
+            tm_st4c<i * 2 * NF + 4 * q>(tw, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+          });
+#elif NLEM_LR_ST == 2
+          static_for<8>([&](auto qc) {
+            constexpr int q = decltype(qc)::value;
+            tm_st2c<i * 2 * NF + 2 * q>(tw, o[2 * q], o[2 * q + 1]);
+          });
+#else
           static_for<16>([&](auto qc) {
             constexpr int q = decltype(qc)::value;
             tm_st1c<i * 2 * NF + q>(tw, o[q]);
           });
+#endif
         });
 #pragma unroll
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
