@@ -287,6 +287,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 
   const float inv_mu = 1.0f / P.mu;
   const bool nlm_init = P.init_mode == NLEM_INIT_NLM_PATCH;
+  const bool irls = P.solver == NLEM_SOLVER_IRLS;
   const int total_warps = gridDim.x * WARPS;
 
   int pix = blockIdx.x * WARPS + warp;
@@ -484,12 +485,88 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       if (lane == 0) gram[R + 2] = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while filling)
       __syncwarp();
     };
-    publish();
     tm_wait_st();
-
     int iters = P.iters;
-    int fw = 0x7fffffff;  // first failure: 2 t (+1 for a non-finite norm)
+    int fw = 0x7fffffff;  // first ADMM failure: 2 t (+1 for a non-finite norm)
     bool ovf = false;
+    int ifail_iter = -1, ifail_kind = 0;  // IRLS failure record
+    if (irls) {
+      // ---- IRLS on the smooth surrogate (proj/include/nlem/irls.hpp:21-68).  Pass p evaluates
+      // at x_p: the surrogate S(x_p) = sum w sqrt(||x_p - a||^2 + eps) and beta_k = w_k / sqrt(..),
+      // then x_{p+1} = sum beta a / sum beta.  Pass 0 gives `previous`; pass t the iteration-t
+      // objective, the stop test (irls.hpp:58) and, if t < T, the next iterate.  Distances are
+      // direct differences (no Gram expansion: exact near coincident points, where eps matters).
+      float previous = 0.0f;
+      int stop_at = -1;
+      for (int pass = 0; pass <= P.iters; ++pass) {
+        if (own0) cb[jy0 * CB_STR + jx0] = own[0];
+        if (own1) cb[jy0 * CB_STR + jx1] = own[32];
+        __syncwarp();
+        float2 d2[SEGL];
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) d2[i] = make_float2(0.0f, 0.0f);
+#pragma unroll 1
+        for (int jx = 0; jx < KS; ++jx) {
+          float nx[KS];
+#pragma unroll
+          for (int jy = 0; jy < KS; ++jy) nx[jy] = -cb[jy * CB_STR + jx];
+          float2 v[SEGL + KS - 1];
+#pragma unroll
+          for (int e = 0; e < SEGL + KS - 1; ++e)
+            v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
+#pragma unroll
+          for (int jy = 0; jy < KS; ++jy)
+#pragma unroll
+            for (int i = 0; i < SEGL; ++i) {
+              const float2 df = __fadd2_rn(v[i + jy], make_float2(nx[jy], nx[jy]));
+              d2[i] = __ffma2_rn(df, df, d2[i]);
+            }
+        }
+        float2 beta[SEGL];
+        float bsum = 0.0f, ssum = 0.0f;
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) {
+          const float rx = sqrtf(d2[i].x + P.epsilon), ry = sqrtf(d2[i].y + P.epsilon);
+          beta[i] = make_float2(wgt[i].x / rx, wgt[i].y / ry);  // irls.hpp:45-46
+          bsum += beta[i].x + beta[i].y;
+          ssum += fmaf(wgt[i].x, rx, wgt[i].y * ry);  // costs.hpp:24-33
+        }
+        float xA, xB, xs[5];
+        {
+          const float ex[5] = {bsum, ssum, 0.0f, 0.0f, 0.0f};
+          patch_sum_reduce(beta, ex, xA, xB, xs);
+        }
+        const float den = xs[0], current = xs[1];
+        const float xnA = xA / den, xnB = xB / den;
+        const bool xbad = __any_sync(0xffffffffu, (own0 && !isfinite(xnA)) || (own1 && !isfinite(xnB)));
+        if (!isfinite(current)) {  // non-finite surrogate at x_pass (irls.hpp:39, :52)
+          ifail_iter = pass;
+          ifail_kind = NLEM_FAIL_IRLS_OBJECTIVE;
+          break;
+        }
+        if (pass >= 1) {
+          if (frames != nullptr && lane == kCenterLane)
+            frames[static_cast<int64_t>(pass - 1) * plane + pix] = box_clamp(own[0], P.range);
+          if (previous - current <= P.irls_tol * fabsf(previous)) {  // irls.hpp:58
+            stop_at = pass;
+            break;
+          }
+        }
+        previous = current;
+        if (pass < P.iters) {
+          if (xbad) {  // non-finite x_{pass+1} (irls.hpp:50)
+            ifail_iter = pass + 1;
+            ifail_kind = NLEM_FAIL_IRLS_ITERATE;
+            break;
+          }
+          if (own0) own[0] = xnA;
+          if (own1) own[32] = xnB;
+        }
+      }
+      // the minimiser is x at the stop pass (or x_T), held in own[0/32]
+      if (ifail_iter < 0) iters = stop_at > 0 ? stop_at : P.iters;
+    } else {
+    publish();
     for (int t = 1; t <= P.iters; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
@@ -635,11 +712,14 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         publish();
       }
     }
+    }  // ADMM
     tm_wait_st();
     const bool any_ovf = __any_sync(0xffffffffu, ovf);
     if (any_ovf) {
       // a dropped history term would have been significant: the exact p-form kernel redoes it
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = pix;
+    } else if (ifail_iter >= 0) {
+      if (lane == 0) record_failure(fail, static_cast<int64_t>(r) * cols + c, ifail_iter, ifail_kind);
     } else if (fw != 0x7fffffff) {
       if (lane == 0) {
         const int tf = fw >> 1;
@@ -647,7 +727,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         record_failure(fail, static_cast<int64_t>(r) * cols + c, fail_iter, NLEM_FAIL_ADMM_ITERATE);
       }
     } else if (lane == kCenterLane) {
-      const float zc = own[0];
+      // NLEM-IRLS clips the unconstrained minimiser (nlem.cpp:53-54); ADMM's z is in the box
+      const float zc = irls ? box_clamp(own[0], P.range) : own[0];
       out[pix] = zc;
       if (frames)
         for (int t = iters; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = zc;
@@ -664,7 +745,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 bool nlem_lr_supported(const NlemLaunch& L) {
   // 32-bit pixel indexing inside the kernel
   const int64_t lim = int64_t(1) << 30;
-  return L.P.solver == NLEM_SOLVER_ADMM && L.P.patch == KS && L.P.search == SW &&
+  return (L.P.solver == NLEM_SOLVER_ADMM || L.P.solver == NLEM_SOLVER_IRLS) && L.P.patch == KS &&
+         L.P.search == SW &&
          L.out_rows * L.cols < lim && L.rows < lim && L.pad_cols < lim;
 }
 
