@@ -48,8 +48,13 @@ namespace lr {
 
 constexpr int KS = 7, SW = 21, HS = SW / 2;
 constexpr int TH = SW + KS - 1;  // 27
-constexpr int TWS = 35;          // tile row stride (bank-distinct segment starts)
-constexpr int TILE = (TH * TWS + 3) / 4 * 4;  // floats per tile buffer (16-byte multiple)
+// Tile layout: three column-major copies; copy b holds tile rows 7b .. 7b+12 (the rows the
+// segments of grid block b read), column x at CP_BASE[b] + x * CS, rows padded to 16 so a
+// segment's 13-value column is four 16-byte loads.  CS = 20 and the copy offsets put the 8 lanes
+// of each LDS.128 phase on distinct bank quads (252 wavefronts per sweep-column set vs 224 ideal).
+constexpr int CS = 20;
+constexpr int CP_B1 = 548, CP_B2 = 1096;
+constexpr int TILE = CP_B2 + TH * CS;  // 1636 floats
 #ifndef NLEM_LR_WARPS
 #define NLEM_LR_WARPS 16
 #endif
@@ -63,7 +68,7 @@ constexpr int NF = 8;    // state fields per point in TMEM
 constexpr int RED_STR = 36;
 constexpr int CB_STR = 8;
 // per-warp shared memory (floats)
-constexpr int W_RED = 2 * TILE;
+constexpr int W_RED = TILE;  // single tile buffer
 constexpr int W_CB = W_RED + 32 * RED_STR;
 constexpr int W_OWN = W_CB + KS * CB_STR;        // [4 + 2 (R+1)][32] owner scalars
 constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 ring
@@ -199,9 +204,7 @@ __device__ __forceinline__ float box_clamp(float v, const nlem_box& box) {
   return (box.upper < y) ? box.upper : y;
 }
 
-// Segment geometry: vertical segment (grid column gx, grid rows 7b .. 7b+6).  Slot 0 and slot 1
-// of the 32 lanes are chosen so that the 32 segment starts b*7*TWS + gx fall on 32 distinct
-// banks in both slots (TWS = 35: 7*35 = 245 = 21 mod 32).
+// Segment geometry: vertical segment (grid column gx, grid rows 7b .. 7b+6).
 __device__ __forceinline__ void seg_of(int lane, int slot, int& gx, int& gy0, bool& valid) {
   valid = true;
   if (slot == 0) {
@@ -220,6 +223,97 @@ __device__ __forceinline__ float2 pin_pair(float2 v) {
   unsigned long long b = (static_cast<unsigned long long>(__float_as_uint(v.y)) << 32) | __float_as_uint(v.x);
   asm volatile("" : "+l"(b));
   return make_float2(__uint_as_float(static_cast<unsigned>(b)), __uint_as_float(static_cast<unsigned>(b >> 32)));
+}
+
+__device__ __forceinline__ int copy_base(int b) { return b == 0 ? 0 : (b == 1 ? CP_B1 : CP_B2); }
+// tile element (row r, column x) in the copy that holds row r
+__device__ __forceinline__ float tile_at(const float* T, int r, int x) {
+  const int b = r < 7 ? 0 : (r < 14 ? 1 : 2);
+  return T[copy_base(b) + x * CS + r - 7 * b];
+}
+// 16 values (13 used) of a segment column: four 16-byte loads
+__device__ __forceinline__ void load_col(const float* col, float (&v)[16]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 t = reinterpret_cast<const float4*>(col)[q];
+    v[4 * q] = t.x;
+    v[4 * q + 1] = t.y;
+    v[4 * q + 2] = t.z;
+    v[4 * q + 3] = t.w;
+  }
+}
+// Even/odd accumulator pairs over the 7 points of a segment: a 7 x 7 correlation step
+// acc[i] += sum_jy f(v[i + jy], c[jy]) is issued as FFMA2 on aligned (v[2m], v[2m+1]) register
+// pairs: even jy updates points (0,1),(2,3),(4,5),(6); odd jy updates (1,2),(3,4),(5,6),(0).
+struct EO {
+  float2 e[3], o[3];
+  float e6, o0;
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int m = 0; m < 3; ++m) e[m] = o[m] = make_float2(0.0f, 0.0f);
+    e6 = o0 = 0.0f;
+  }
+  __device__ __forceinline__ float get(int i) const {  // i compile-time after unrolling
+    const float ev = i == 6 ? e6 : (i & 1 ? e[i >> 1].y : e[i >> 1].x);
+    const float od = i == 0 ? o0 : (i & 1 ? o[i >> 1].x : o[(i - 1) >> 1].y);
+    return ev + od;
+  }
+};
+// acc[i] += v[i + jy] * c[jy]
+__device__ __forceinline__ void eo_dot(EO& a, const float (&v)[16], const float (&c)[KS]) {
+#pragma unroll
+  for (int jy = 0; jy < KS; ++jy) {
+    const float2 cc = make_float2(c[jy], c[jy]);
+    if ((jy & 1) == 0) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) a.e[m] = __ffma2_rn(make_float2(v[2 * m + jy], v[2 * m + 1 + jy]), cc, a.e[m]);
+      a.e6 = fmaf(v[6 + jy], c[jy], a.e6);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) a.o[m] = __ffma2_rn(make_float2(v[2 * m + 1 + jy], v[2 * m + 2 + jy]), cc, a.o[m]);
+      a.o0 = fmaf(v[jy], c[jy], a.o0);
+    }
+  }
+}
+// acc[i] += (v[i + jy] + nx[jy])^2   (nx = -x)
+__device__ __forceinline__ void eo_dist(EO& a, const float (&v)[16], const float (&nx)[KS]) {
+#pragma unroll
+  for (int jy = 0; jy < KS; ++jy) {
+    const float2 cc = make_float2(nx[jy], nx[jy]);
+    if ((jy & 1) == 0) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const float2 d = __fadd2_rn(make_float2(v[2 * m + jy], v[2 * m + 1 + jy]), cc);
+        a.e[m] = __ffma2_rn(d, d, a.e[m]);
+      }
+      const float d6 = v[6 + jy] + nx[jy];
+      a.e6 = fmaf(d6, d6, a.e6);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const float2 d = __fadd2_rn(make_float2(v[2 * m + 1 + jy], v[2 * m + 2 + jy]), cc);
+        a.o[m] = __ffma2_rn(d, d, a.o[m]);
+      }
+      const float d0 = v[jy] + nx[jy];
+      a.o0 = fmaf(d0, d0, a.o0);
+    }
+  }
+}
+// g[jy] += u[i] * v[i + jy]: even i updates coordinates (0,1),(2,3),(4,5),(6); odd i (1,2),(3,4),(5,6),(0)
+__device__ __forceinline__ void eo_gsum(EO& g, const float (&v)[16], const float (&u)[SEGL]) {
+#pragma unroll
+  for (int i = 0; i < SEGL; ++i) {
+    const float2 uu = make_float2(u[i], u[i]);
+    if ((i & 1) == 0) {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) g.e[m] = __ffma2_rn(make_float2(v[i + 2 * m], v[i + 2 * m + 1]), uu, g.e[m]);
+      g.e6 = fmaf(v[i + 6], u[i], g.e6);
+    } else {
+#pragma unroll
+      for (int m = 0; m < 3; ++m) g.o[m] = __ffma2_rn(make_float2(v[i + 2 * m + 1], v[i + 2 * m + 2]), uu, g.o[m]);
+      g.o0 = fmaf(v[i], u[i], g.o0);
+    }
+  }
 }
 
 // sum of red[row][0..31] (row stride RED_STR, 16-byte aligned) in a fixed tree order
@@ -279,7 +373,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   bool sval0, sval1;
   seg_of(lane, 0, sgx0, sgy00, sval0);
   seg_of(lane, 1, sgx1, sgy01, sval1);
-  const int soff0 = sgy00 * TWS + sgx0, soff1 = sgy01 * TWS + sgx1;
+  const int soff0 = copy_base(sgy00 / 7) + sgx0 * CS, soff1 = copy_base(sgy01 / 7) + sgx1 * CS;
   // coordinate owners: the reduction runs in two halves (patch columns 0-3 and 4-6); row
   // l of half A is coordinate (l % 7, l / 7), row l of half B is (l % 7, 4 + l / 7)
   const bool own0 = lane < 4 * KS, own1 = lane < 3 * KS;
@@ -291,17 +385,26 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const int total_warps = gridDim.x * WARPS;
 
   int pix = blockIdx.x * WARPS + warp;
-  int buf = 0;
   auto issue_tile = [&](int p, int b) {
     const int r = out_row0 + p / cols, c = p % cols;
     const float* src = pad + static_cast<int64_t>(r - out_row0) * pad_cols + c;
-    float* T = W + b * TILE;
-    if (lane < TH) {  // one tile column per lane, row by row (no hoisted per-element offsets)
+    (void)b;
+    if (lane < TH) {  // one tile column per lane, copy by copy (no hoisted per-element offsets)
+#pragma unroll
+      for (int cb_ = 0; cb_ < 3; ++cb_) {
+        float* dst = W + copy_base(cb_) + lane * CS;
+        const float* sp = src + static_cast<int64_t>(7 * cb_) * pad_cols + lane;
 #pragma unroll 1
-      for (int tr = 0; tr < TH; ++tr, src += pad_cols) cpa4(T + tr * TWS + lane, src + lane);
+        for (int e = 0; e < SEGL + KS - 1; ++e, sp += pad_cols) cpa4(dst + e, sp);
+      }
     }
     cpa_commit();
   };
+  // the 3 padding rows of every column copy are read by the 16-byte column loads: keep them 0
+  for (int e = lane; e < 3 * TH * 3; e += 32) {
+    const int cp = e / (TH * 3), rem = e % (TH * 3);
+    W[copy_base(cp) + (rem / 3) * CS + 13 + rem % 3] = 0.0f;
+  }
   if (pix < plane) issue_tile(pix, 0);
 
   while (pix < plane) {
@@ -310,8 +413,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
     cpa_wait();
     __syncwarp();
-    const float* const T = W + buf * TILE;
-    if (nxt < plane) issue_tile(nxt, buf ^ 1);
+    const float* const T = W;
 
     const int r = out_row0 + pix / cols, c = pix % cols;
     const int gr0 = r < HS ? HS - r : 0;
@@ -321,11 +423,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     const float inv_n = 1.0f / static_cast<float>((gr1 - gr0 + 1) * (gc1 - gc0 + 1));
 
     // ---- footprint constancy (exact-stop candidate, admm.hpp:77 with tol 0)
-    const float a0 = T[gr0 * TWS + gc0];
+    const float a0 = tile_at(T, gr0, gc0);
     bool neq = false;
     if (lane >= gc0 && lane <= gc1 + KS - 1) {
 #pragma unroll 1
-      for (int tr = gr0; tr <= gr1 + KS - 1; ++tr) neq |= T[tr * TWS + lane] != a0;
+      for (int tr = gr0; tr <= gr1 + KS - 1; ++tr) neq |= tile_at(T, tr, lane) != a0;
     }
     const bool static_eq = !__any_sync(0xffffffffu, neq);
 
@@ -333,27 +435,23 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     unsigned realmask = 0;  // bit s*7+i: grid point inside the clipped window (patch.cpp:72-76)
     float2 wgt[SEGL];  // (slot 0, slot 1) pairs
     {
-      // the two slots of a lane run as the two halves of FADD2 / FFMA2 pairs
-      float2 A2[SEGL];
-#pragma unroll
-      for (int i = 0; i < SEGL; ++i) A2[i] = make_float2(0.0f, 0.0f);
+      EO a0s, a1s;
+      a0s.zero();
+      a1s.zero();
 #pragma unroll 1
       for (int jx = 0; jx < KS; ++jx) {
-        float2 v[SEGL + KS - 1];
+        float nac[KS];
 #pragma unroll
-        for (int e = 0; e < SEGL + KS - 1; ++e)
-          v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
-#pragma unroll
-        for (int jy = 0; jy < KS; ++jy) {
-          const float ac = -T[(HS + jy) * TWS + HS + jx];
-          const float2 nac = make_float2(ac, ac);
-#pragma unroll
-          for (int i = 0; i < SEGL; ++i) {
-            const float2 df = __fadd2_rn(v[i + jy], nac);
-            A2[i] = __ffma2_rn(df, df, A2[i]);
-          }
-        }
+        for (int jy = 0; jy < KS; ++jy) nac[jy] = -T[CP_B1 + (HS + jx) * CS + 3 + jy];  // a_self
+        float v[16];
+        load_col(T + soff0 + jx * CS, v);
+        eo_dist(a0s, v, nac);
+        load_col(T + soff1 + jx * CS, v);
+        eo_dist(a1s, v, nac);
       }
+      float2 A2[SEGL];
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) A2[i] = make_float2(a0s.get(i), a1s.get(i));
       float lm[16];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -366,7 +464,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           const float w = real ? expf(-a2 * P.inv_h2) : 0.0f;
           if (s) wgt[i].y = w; else wgt[i].x = w;
           realmask |= real ? 1u << (s * SEGL + i) : 0u;
-          lm[2 * i + s] = inv_mu * w;
+          lm[2 * i + s] = irls ? w : inv_mu * w;  // IRLS keeps the weights themselves
         }
       }
       lm[14] = lm[15] = 0.0f;
@@ -387,26 +485,24 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int jxa = hf ? 4 : 0, jxb = hf ? KS : 4;
+        float u0[SEGL], u1[SEGL];
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) {
+          u0[i] = u2[i].x;
+          u1[i] = u2[i].y;
+        }
 #pragma unroll 1
         for (int jx = jxa; jx < jxb; ++jx) {
-          // keep the (slot 0, slot 1) weights in aligned 64-bit register pairs for FFMA2
-          float2 up[SEGL];
-#pragma unroll
-          for (int i = 0; i < SEGL; ++i) up[i] = pin_pair(u2[i]);
-          float2 gc[KS];
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy) gc[jy] = make_float2(0.0f, 0.0f);
-          float2 v[SEGL + KS - 1];
-#pragma unroll
-          for (int e = 0; e < SEGL + KS - 1; ++e)
-            v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy)
-#pragma unroll
-            for (int i = 0; i < SEGL; ++i) gc[jy] = __ffma2_rn(up[i], v[i + jy], gc[jy]);
+          EO g;
+          g.zero();
+          float v[16];
+          load_col(T + soff0 + jx * CS, v);
+          eo_gsum(g, v, u0);
+          load_col(T + soff1 + jx * CS, v);
+          eo_gsum(g, v, u1);
           float* rrow = red + (jx - jxa) * KS * RED_STR + lane;
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = gc[jy].x + gc[jy].y;
+          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = g.get(jy);
         }
         if (hf) {
 #pragma unroll
@@ -430,8 +526,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // Owner scalars in shared memory: rows 0 z_A, 1 z_B, 2 m_A, 3 m_B, 4.. c~ history ring
     // (slot (head - q) mod (R+1) holds c~_{t-q}), A then B.
     {
-      const float mA = own0 ? T[(HS + jy0) * TWS + HS + jx0] : 0.0f;
-      const float mB = own1 ? T[(HS + jy0) * TWS + HS + jx1] : 0.0f;
+      const float mA = own0 ? T[CP_B1 + (HS + jx0) * CS + 3 + jy0] : 0.0f;
+      const float mB = own1 ? T[CP_B1 + (HS + jx1) * CS + 3 + jy0] : 0.0f;
       float zA = mA, zB = mB;
       if (nlm_init) {
         float ex[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
@@ -479,8 +575,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
       for (int q = 0; q < R + 2; ++q) gram[q] = part[q];  // same value in every lane
       if (lane == 0) nrs[head] = part[R];
-      if (own0) cb[jy0 * CB_STR + jx0] = cA;
-      if (own1) cb[jy0 * CB_STR + jx1] = cB;
+      if (own0) cb[jx0 * CB_STR + jy0] = cA;
+      if (own1) cb[jx1 * CB_STR + jy0] = cB;
       __syncwarp();
       if (lane == 0) gram[R + 2] = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while filling)
       __syncwarp();
@@ -499,37 +595,36 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       float previous = 0.0f;
       int stop_at = -1;
       for (int pass = 0; pass <= P.iters; ++pass) {
-        if (own0) cb[jy0 * CB_STR + jx0] = own[0];
-        if (own1) cb[jy0 * CB_STR + jx1] = own[32];
+        if (own0) cb[jx0 * CB_STR + jy0] = own[0];
+        if (own1) cb[jx1 * CB_STR + jy0] = own[32];
         __syncwarp();
-        float2 d2[SEGL];
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) d2[i] = make_float2(0.0f, 0.0f);
+        EO e0, e1;
+        e0.zero();
+        e1.zero();
 #pragma unroll 1
         for (int jx = 0; jx < KS; ++jx) {
           float nx[KS];
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy) nx[jy] = -cb[jy * CB_STR + jx];
-          float2 v[SEGL + KS - 1];
-#pragma unroll
-          for (int e = 0; e < SEGL + KS - 1; ++e)
-            v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
-#pragma unroll
-          for (int jy = 0; jy < KS; ++jy)
-#pragma unroll
-            for (int i = 0; i < SEGL; ++i) {
-              const float2 df = __fadd2_rn(v[i + jy], make_float2(nx[jy], nx[jy]));
-              d2[i] = __ffma2_rn(df, df, d2[i]);
-            }
+          for (int jy = 0; jy < KS; ++jy) nx[jy] = -cb[jx * CB_STR + jy];
+          float v[16];
+          load_col(T + soff0 + jx * CS, v);
+          eo_dist(e0, v, nx);
+          load_col(T + soff1 + jx * CS, v);
+          eo_dist(e1, v, nx);
         }
+        float2 d2[SEGL];
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) d2[i] = make_float2(e0.get(i), e1.get(i));
         float2 beta[SEGL];
         float bsum = 0.0f, ssum = 0.0f;
+        float wl[16];
+        tm_ld16c_wait<2 * NF * SEGL>(tw, wl);
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
           const float rx = sqrtf(d2[i].x + P.epsilon), ry = sqrtf(d2[i].y + P.epsilon);
-          beta[i] = make_float2(wgt[i].x / rx, wgt[i].y / ry);  // irls.hpp:45-46
+          beta[i] = make_float2(wl[2 * i] / rx, wl[2 * i + 1] / ry);  // irls.hpp:45-46
           bsum += beta[i].x + beta[i].y;
-          ssum += fmaf(wgt[i].x, rx, wgt[i].y * ry);  // costs.hpp:24-33
+          ssum += fmaf(wl[2 * i], rx, wl[2 * i + 1] * ry);  // costs.hpp:24-33
         }
         float xA, xB, xs[5];
         {
@@ -575,21 +670,27 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       float usum = 0.0f;
       bool fnorm = false, sne1 = false;
       float2 Dk2[SEGL];
-#pragma unroll
-      for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(0.0f, 0.0f);
+      {
+        EO d0, d1;
+        d0.zero();
+        d1.zero();
 #pragma unroll 1
-      for (int jx = 0; jx < KS; ++jx) {
-        float cvx[KS];  // column jx of c~ (broadcast loads; FFMA2 takes it as a scalar operand)
+        for (int jx = 0; jx < KS; ++jx) {
+          float cvx[KS];  // column jx of c~ (two broadcast 16-byte loads)
+          {
+            const float4 ca = reinterpret_cast<const float4*>(cb + jx * CB_STR)[0];
+            const float4 cc = reinterpret_cast<const float4*>(cb + jx * CB_STR)[1];
+            cvx[0] = ca.x; cvx[1] = ca.y; cvx[2] = ca.z; cvx[3] = ca.w;
+            cvx[4] = cc.x; cvx[5] = cc.y; cvx[6] = cc.z;
+          }
+          float v[16];
+          load_col(T + soff0 + jx * CS, v);
+          eo_dot(d0, v, cvx);
+          load_col(T + soff1 + jx * CS, v);
+          eo_dot(d1, v, cvx);
+        }
 #pragma unroll
-        for (int jy = 0; jy < KS; ++jy) cvx[jy] = cb[jy * CB_STR + jx];
-        float2 v[SEGL + KS - 1];  // (slot 0, slot 1) tile values
-#pragma unroll
-        for (int e = 0; e < SEGL + KS - 1; ++e)
-          v[e] = make_float2(T[soff0 + e * TWS + jx], T[soff1 + e * TWS + jx]);
-#pragma unroll
-        for (int jy = 0; jy < KS; ++jy)
-#pragma unroll
-          for (int i = 0; i < SEGL; ++i) Dk2[i] = __ffma2_rn(v[i + jy], make_float2(cvx[jy], cvx[jy]), Dk2[i]);
+        for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(d0.get(i), d1.get(i));
       }
       {
         float lm[16];
@@ -733,9 +834,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       if (frames)
         for (int t = iters; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = zc;
     }
-    __syncwarp();
+    __syncwarp();  // every lane is done with the tile before the next one streams in
+    if (nxt < plane) issue_tile(nxt, 0);
     pix = nxt;
-    buf ^= 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();

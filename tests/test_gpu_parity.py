@@ -429,12 +429,12 @@ def test_lr_kernel_matches_tile_kernel(nb, tmp_path):
     lr = _run_forced_kernel("lr", noisy, kw, tmp_path)
     tile = _run_forced_kernel("tile", noisy, kw, tmp_path)
     assert np.abs(lr - tile).max() <= 2e-3
-    # IRLS surrogate solver (fixed count, tol < 0, and the reference's tol = 0 stall rule)
-    for tol in (-1.0, 0.0):
-        kwi = dict(kw, solver="irls", epsilon=1e-4, irls_tol=tol)
-        lr = _run_forced_kernel("lr", noisy, kwi, tmp_path)
-        tile = _run_forced_kernel("tile", noisy, kwi, tmp_path)
-        assert np.abs(lr - tile).max() <= 2e-3
+    # IRLS surrogate solver at a fixed count (tol < 0: the FP32 stall point of the tol = 0 rule
+    # depends on rounding order)
+    kwi = dict(kw, solver="irls", epsilon=1e-4, irls_tol=-1.0)
+    lr = _run_forced_kernel("lr", noisy, kwi, tmp_path)
+    tile = _run_forced_kernel("tile", noisy, kwi, tmp_path)
+    assert np.abs(lr - tile).max() <= 2e-3
     img = np.zeros((30, 30), np.float32)
     img[12:18, 12:18] = np.where(np.add.outer(np.arange(6), np.arange(6)) % 2 == 0, 0.0, 3e19)
     kw = dict(search=21, patch=7, h=1e30, sigma=10.0, solver="admm", solver_iters=4, mu=1.0,
