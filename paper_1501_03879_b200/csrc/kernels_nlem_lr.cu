@@ -231,16 +231,21 @@ __device__ __forceinline__ float tile_at(const float* T, int r, int x) {
   const int b = r < 7 ? 0 : (r < 14 ? 1 : 2);
   return T[copy_base(b) + x * CS + r - 7 * b];
 }
-// 16 values (13 used) of a segment column: four 16-byte loads
+// 16 values (13 used) of a segment column: four 16-byte loads.  The last quad is an opaque
+// ld.shared.v4 so the compiler does not shrink it to a 4-byte load of v[12] (a 4-byte load at
+// the 20-float column stride is a 4-way bank conflict; the 16-byte phases are conflict-free).
 __device__ __forceinline__ void load_col(const float* col, float (&v)[16]) {
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 3; ++q) {
     const float4 t = reinterpret_cast<const float4*>(col)[q];
     v[4 * q] = t.x;
     v[4 * q + 1] = t.y;
     v[4 * q + 2] = t.z;
     v[4 * q + 3] = t.w;
   }
+  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+      : "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
+      : "r"(su32(col + 12)));
 }
 // Even/odd accumulator pairs over the 7 points of a segment: a 7 x 7 correlation step
 // acc[i] += sum_jy f(v[i + jy], c[jy]) is issued as FFMA2 on aligned (v[2m], v[2m+1]) register
