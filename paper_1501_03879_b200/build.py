@@ -36,7 +36,12 @@ def _stale() -> bool:
     t = os.path.getmtime(SO)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
     deps.append(os.path.join(os.path.dirname(HERE), "include", "nlem_b200.h"))
-    return any(os.path.getmtime(p) > t for p in deps)
+    if not os.path.exists(os.path.join(OUT_DIR, "nlem")):
+        return True
+    cli_deps = [os.path.join(HERE, "cli", "nlem_main.cpp"),
+                os.path.join(os.path.dirname(HERE), "include", "nlem_b200.hpp"),
+                os.path.join(os.path.dirname(HERE), "include", "nlem_b200_io.hpp")]
+    return any(os.path.getmtime(p) > t for p in deps + cli_deps)
 
 
 # experimental build variants (A/B and debug only): "_"-separated tokens -> defines
@@ -93,7 +98,25 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     os.replace(tmp, so)
     for o in objs:
         os.remove(o)
+    if not variant:
+        build_cli(verbose)
     return so
+
+
+CLI_SRC = os.path.join(HERE, "cli", "nlem_main.cpp")
+CLI_BIN = os.path.join(OUT_DIR, "nlem")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """The `nlem` command-line front end (host C++ over the C-ABI library, rpath $ORIGIN)."""
+    inc = os.path.join(os.path.dirname(HERE), "include")
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", inc, CLI_SRC, "-o", CLI_BIN + ".tmp",
+           "-L", OUT_DIR, "-lnlem_b200", "-Wl,-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(CLI_BIN + ".tmp", CLI_BIN)
+    return CLI_BIN
 
 
 if __name__ == "__main__":
