@@ -62,6 +62,15 @@ constexpr int WARPS = NLEM_LR_WARPS;  // pixel-warps per CTA (1 CTA per SM)
 constexpr int SEGL = 7;  // points per segment
 constexpr int R = 4;     // history ring
 constexpr int NF = 8;    // state fields per point in TMEM
+// unroll factors of the correlation loops over patch columns (A/B build variants)
+#ifndef NLEM_LR_UD
+#define NLEM_LR_UD 1
+#endif
+#ifndef NLEM_LR_UG
+#define NLEM_LR_UG 1
+#endif
+#define LR_PRAGMA(x) _Pragma(#x)
+#define LR_UNROLL(n) LR_PRAGMA(unroll n)
 #ifndef NLEM_LR_ST
 #define NLEM_LR_ST 2  // columns per tcgen05.st in the sweep (1, 2 or 4)
 #endif
@@ -496,7 +505,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           u0[i] = u2[i].x;
           u1[i] = u2[i].y;
         }
-#pragma unroll 1
+        LR_UNROLL(NLEM_LR_UG)
         for (int jx = jxa; jx < jxb; ++jx) {
           EO g;
           g.zero();
@@ -679,7 +688,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         EO d0, d1;
         d0.zero();
         d1.zero();
-#pragma unroll 1
+        LR_UNROLL(NLEM_LR_UD)
         for (int jx = 0; jx < KS; ++jx) {
           float cvx[KS];  // column jx of c~ (two broadcast 16-byte loads)
           {
