@@ -359,7 +359,28 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
                cfg.mu, cfg.max_iter, cfg.tol_primal,
                res_mode_for(cfg.tol_primal, trace_residual != nullptr), z_out, objective_out,
                iters_out, trace_objective, trace_residual, reinterpret_cast<FailureSlot*>(slot.ptr)};
-  e = admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
+  if (admm_lr_supported(L)) {
+    // low-rank kernel, then the exact p-form kernel over the problems it handed off
+    int* scratch = nullptr;  // [0] hand-off count, [1..] hand-off list
+    e = cudaMallocAsync(&scratch, (1 + batch) * sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = launch_admm_lr(L, scratch + 1, scratch, s);
+    if (e == cudaSuccess) e = launch_admm_fast_list(L, scratch + 1, scratch, s);
+    const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;  // read per call (tests)
+    if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
+      int handed = 0;
+      e = cudaMemcpyAsync(&handed, scratch, sizeof(int), cudaMemcpyDeviceToHost, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      std::fprintf(stderr, "admm_lr: %lld problems, %d handed to the p-form kernel\n",
+                   static_cast<long long>(batch), handed);
+    }
+    if (scratch) {
+      const cudaError_t ef = cudaFreeAsync(scratch, s);
+      if (e == cudaSuccess) e = ef;
+    }
+  } else {
+    e = admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
+  }
   if (e != cudaSuccess) return cuda_fail(failure, e);
   if (!failure) return NLEM_OK;
   unsigned long long v = ~0ull;

@@ -1,0 +1,489 @@
+// Low-rank (Gram-form) EM-ADMM for batched standalone solves, d = 49, 3 <= n <= 448
+// (BASELINE config 1: 65,536 problems x n = 441 x d = 49).
+//
+// Algebra: the p-form of admm.hpp:49-78 unrolled as in kernels_nlem_lr.cu.  With everything
+// centred on m = z_0 (the initial consensus: the weighted mean, admm.hpp:40, or z_init),
+//     s_k p_k = sum_r al_r c~_{t-r} - ga a~_k,     a~ = a - m,  c~ = c - m,
+// so a point carries 8 scalars (H = ||s p - a~||^2, K = <s p - a~, a~>, ga, ||a~||^2, al_0..3)
+// and a sweep is one dot product D_k = <a~_k, c~_t> plus one weighted sum sum_k ga'_k a~_k:
+//     N = H + 2 (sum_r al_r <c~_{t-1-r}, c~_t> - (ga + 1) D) + ||c~_t||^2        (= ||p_k||^2)
+//     s = min(1, lambda rsqrt N), B = K + D, H' = s (s N - 2B) + ||a~||^2, K' = s B - ||a~||^2,
+//     ga' = s (ga + 1), al' = (s, s al_0, s al_1, s al_2)
+//     z_t = P_C(z_{t-1} - g/n),  g = sum_r (sum_k al'_r) c~_{t-r} - sum_k ga'_k a~_k,
+//     c~_{t+1} = 2 z_t - z_{t-1} - m.
+// A problem whose history ring would drop a term above FP32 rounding of p (2^-22 ||p||), whose
+// points are all equal (the exact-stop case of admm.hpp:77, tested structurally by the p-form
+// kernel), or that produces a non-finite value is handed, through a device-side list, to the
+// exact p-form kernel (admm_batched_fast), which then owns its outputs and failure record.
+//
+// Mapping (B200): one problem per CTA of 14 warps, 1 CTA per SM.
+//  * the centred points live in REGISTERS (the p-form kernel kept them in shared memory and
+//    re-read them every sweep): groups of 8 lanes own 8 points, each lane 7 coordinates
+//    (j = 8 i + g, d padded to 56) as float2 point pairs, so both passes are FFMA2;
+//  * lane g of a group owns the scalar state of point slot g: reduce-scatter of the 8 dot
+//    products in the group, scalar update, all-gather of ga';
+//  * one CTA barrier per sweep: per-warp column partials (double-buffered rows), then EVERY
+//    warp redundantly finishes the consensus for all coordinates (lane l: j = l, l + 32) in the
+//    same fixed order, so all warps hold bitwise identical z, c~ and Gram rows without a second
+//    barrier;
+//  * the next problem's points and weights stream into a shared-memory staging buffer with
+//    16-byte cp.async during the current problem's sweeps.
+#include <algorithm>
+#include <cstdint>
+#include <cstdlib>
+#include <string>
+
+#include "launch.h"
+
+namespace nlemk {
+
+namespace blr {
+
+constexpr int D = 49, G = 8, J = 7, KP = G / 2;
+constexpr int WARPS = 14, THREADS = 32 * WARPS;
+constexpr int GPW = 32 / G, NG = GPW * WARPS, NCAP = NG * G;  // 56 groups, 448 points
+constexpr int R = 4;
+// Column layout of every per-coordinate row (partials, c~, m): lane g of a group owns
+// coordinates j = 7 g + i (i < 7) at columns 8 g + i; column 8 g + 7 carries the history sum
+// sum_k al'_g for g < 4 (partial rows) and is 0 otherwise.
+constexpr int RS = 64;
+constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2: ring term below FP32 rounding
+constexpr float kCancel = 1.0f / 256.0f;           // N below 2^-8 (H + ||c~||^2): cancellation
+// shared memory (floats)
+constexpr int SM_STAGE = 0;                      // raw points of the next problem (+4 shift)
+constexpr int SM_WST = SM_STAGE + NCAP * D + 4;  // raw weights of the next problem (+4 shift)
+constexpr int SM_RED = SM_WST + NCAP + 4;        // [WARPS][RS] per-warp partial rows
+constexpr int SM_CB = SM_RED + WARPS * RS;       // [RS] c~ of the coming sweep
+constexpr int SM_MB = SM_CB + RS;                // [RS] m (centring), then z~ for the cost
+constexpr int SM_GR = SM_MB + RS;                // [8] Gram row: G_0..G_3, ||c~||^2, ||c~_{t-4}||^2
+constexpr int SM_SCAL = SM_GR + 8;               // [32] block-sum scratch
+constexpr int SM_TOTAL = SM_SCAL + 32;
+constexpr size_t SMEM_BYTES = size_t(SM_TOTAL) * sizeof(float);
+static_assert(NCAP >= 441, "config-1 capacity");
+static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_GR % 4 == 0, "alignment");
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ float rsq(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+
+// element e of `src` lands at dst[shift(src) + e], shift = (src / 4) mod 4, so that global and
+// shared addresses agree mod 16 and the interior moves as 16-byte cp.async
+__device__ __forceinline__ int stage_shift(const float* src) {
+  return static_cast<int>((reinterpret_cast<uintptr_t>(src) >> 2) & 3);
+}
+__device__ __forceinline__ void stage_copy(float* dst, const float* src, int total) {
+  const int s0 = stage_shift(src);
+  const int nch = (s0 + total + 3) >> 2;
+  const float* base = src - s0;  // 16-byte aligned
+  for (int c = threadIdx.x; c < nch; c += THREADS) {
+    const int e0 = 4 * c - s0;
+    if (e0 >= 0 && e0 + 3 < total) {
+      cp16(dst + 4 * c, base + 4 * c);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q;
+        if (e >= 0 && e < total) cp4(dst + 4 * c + q, base + 4 * c + q);
+      }
+    }
+  }
+}
+
+// Reduce-scatter of 8 per-point values (4 float2 slots) across the 8 lanes of a group: lane g
+// returns the sum for point slot g.  Fixed tree (bitwise deterministic).
+__device__ __forceinline__ float group_rs8(const float2 (&v)[KP], int g) {
+  float x[G];
+#pragma unroll
+  for (int m = 0; m < KP; ++m) {
+    x[2 * m] = v[m].x;
+    x[2 * m + 1] = v[m].y;
+  }
+#pragma unroll
+  for (int half = G / 2; half >= 1; half >>= 1) {
+    const bool up = (g & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float keep = up ? x[i + half] : x[i];
+      const float send = up ? x[i] : x[i + half];
+      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return x[0];
+}
+// All-gather of one value per lane of the group into 4 float2 slots (slot 2m, 2m+1).
+__device__ __forceinline__ void group_ag8(float mine, float2 (&out)[KP], int lane) {
+  const int base = lane & ~(G - 1);
+#pragma unroll
+  for (int m = 0; m < KP; ++m) {
+    out[m].x = __shfl_sync(0xffffffffu, mine, base + 2 * m);
+    out[m].y = __shfl_sync(0xffffffffu, mine, base + 2 * m + 1);
+  }
+}
+// Sum the 7 per-lane column partials over the 4 groups of the warp (lanes of group 0 then
+// hold the warp totals of their coordinates) and write them, with v7 in column 8 g + 7, as the
+// warp's partial row (two 16-byte stores per lane of group 0).
+__device__ __forceinline__ void fold_store(float (&v)[J], float v7, float* row, int lane) {
+#pragma unroll
+  for (int o = G; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < J; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+  if (lane < G) {
+    float4* d = reinterpret_cast<float4*>(row + 8 * lane);
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v7);
+  }
+}
+// Column pair (2 lane, 2 lane + 1) summed over the WARPS partial rows in a fixed tree.
+__device__ __forceinline__ float2 rows_sum(const float* red, int lane) {
+  float2 r[WARPS];
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) r[w] = reinterpret_cast<const float2*>(red + w * RS)[lane];
+#pragma unroll
+  for (int span = 1; span < WARPS; span <<= 1)
+#pragma unroll
+    for (int w = 0; w + span < WARPS; w += 2 * span) r[w] = __fadd2_rn(r[w], r[w + span]);
+  return r[0];
+}
+// the 7 coordinates (8 columns) of lane g of a group from a published row
+__device__ __forceinline__ void load_coords(const float* row, int g, float (&c)[J]) {
+  const float4 a = reinterpret_cast<const float4*>(row + 8 * g)[0];
+  const float4 b = reinterpret_cast<const float4*>(row + 8 * g)[1];
+  c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
+  c[4] = b.x; c[5] = b.y; c[6] = b.z;
+}
+// Block sum of one value per thread (fixed order).  Contains two barriers.
+__device__ __forceinline__ float block_sum(float v, float* scal, int warp, int lane) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) scal[warp] = v;
+  __syncthreads();
+  float t = 0.0f;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) t += scal[w];
+  __syncthreads();
+  return t;
+}
+
+}  // namespace blr
+
+using namespace blr;
+
+__global__ void __launch_bounds__(THREADS, 1)
+admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
+                int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
+                int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
+                int* ho_count) {
+  extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
+  float* const red = smem + SM_RED;
+  float* const cb = smem + SM_CB;
+  float* const mb = smem + SM_MB;
+  float* const gr = smem + SM_GR;
+  float* const scal = smem + SM_SCAL;
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int lane = tid & 31;
+  const int g = lane & (G - 1);
+  const int gid = warp * GPW + (lane >> 3);
+  float* const myrow = red + warp * RS;
+  // point of slot q of this lane's group: pair m = q / 2 is point pair m * NG + gid
+  auto point_of = [&](int q) { return 2 * ((q >> 1) * NG + gid) + (q & 1); };
+  const int k_me = point_of(g);
+  const bool real_me = k_me < n;
+  // consensus (warp 0): lane l finishes columns 2l, 2l+1 = coordinates cj, cj + 1
+  const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
+  const int cj = 7 * cgrp + cidx;
+  const bool cv0 = cgrp < 7, cv1 = cgrp < 7 && (lane & 3) != 3;
+  const float inv_mu = 1.0f / mu;
+  const float inv_n = 1.0f / static_cast<float>(n);
+  const int nd = n * D;
+
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+
+  for (; b < batch; b += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();
+    // ---- this problem's points (raw) into registers, weights, all-equal test
+    const float* const src = points + b * nd;
+    const float* const st = stage + stage_shift(src);
+    const float* const wv = wst + stage_shift(weights + b * n);
+    float2 A[KP][J];
+    float2 wq[KP];
+    int neq = 0;
+#pragma unroll
+    for (int m = 0; m < KP; ++m) {
+      const int k0 = 2 * (m * NG + gid), k1 = k0 + 1;
+      wq[m] = make_float2(k0 < n ? wv[k0] : 0.0f, k1 < n ? wv[k1] : 0.0f);
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        const int j = 7 * g + i;
+        float v0 = 0.0f, v1 = 0.0f;
+        if (j < D) {
+          const float r0 = st[j];
+          if (k0 < n) v0 = st[k0 * D + j];
+          if (k1 < n) v1 = st[k1 * D + j];
+          neq |= (k0 < n && v0 != r0) | (k1 < n && v1 != r0);
+        }
+        A[m][i] = make_float2(v0, v1);
+      }
+    }
+    const float w_me = real_me ? wv[k_me] : 0.0f;
+    const bool static_eq = !__syncthreads_or(neq);  // every thread is done with the stage
+    const int64_t bn = b + gridDim.x;
+    if (bn < batch) {
+      stage_copy(stage, points + bn * nd, nd);
+      stage_copy(wst, weights + bn * n, n);
+    }
+    cp_commit();
+    if (static_eq) {  // exact stop possible: the p-form kernel decides it structurally
+      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      continue;
+    }
+
+    // ---- z_0 = m: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
+    float m0 = 0.0f, m1 = 0.0f;  // warp 0: m at coordinates cj, cj + 1
+    if (z_init == nullptr) {
+      const float W = block_sum(w_me, scal, warp, lane);
+      float2 coef[KP];
+#pragma unroll
+      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x / W, wq[m].y / W);
+      float v[J];
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(coef[m], A[m][i], acc);
+        v[i] = acc.x + acc.y;
+      }
+      fold_store(v, 0.0f, myrow, lane);
+      __syncthreads();
+    }
+    if (warp == 0) {
+      if (z_init != nullptr) {
+        m0 = cv0 ? z_init[b * D + cj] : 0.0f;
+        m1 = cv1 ? z_init[b * D + cj + 1] : 0.0f;
+      } else {
+        const float2 s = rows_sum(red, lane);
+        m0 = cv0 ? s.x : 0.0f;
+        m1 = cv1 ? s.y : 0.0f;
+      }
+      reinterpret_cast<float2*>(mb)[lane] = make_float2(m0, m1);
+      reinterpret_cast<float2*>(cb)[lane] = make_float2(0.0f, 0.0f);  // c~_1 = z_0 - m = 0
+      if (lane < 8) gr[lane] = 0.0f;
+    }
+    __syncthreads();
+    // centre the points on m
+    float2 nq[KP];
+    {
+      float mc[J];
+      load_coords(mb, g, mc);
+#pragma unroll
+      for (int m = 0; m < KP; ++m) nq[m] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        const int j = 7 * g + i;
+#pragma unroll
+        for (int m = 0; m < KP; ++m) {
+          const int k0 = 2 * (m * NG + gid);
+          const float2 a = A[m][i];
+          A[m][i] = make_float2(j < D && k0 < n ? a.x - mc[i] : 0.0f,
+                                j < D && k0 + 1 < n ? a.y - mc[i] : 0.0f);
+          nq[m] = __ffma2_rn(A[m][i], A[m][i], nq[m]);
+        }
+      }
+    }
+    const float a2 = group_rs8(nq, g);  // ||a~||^2 of this lane's point
+    // per-point state (own slot): p_1 = z_0 - a = -a~ (u = 0, admm.hpp:41)
+    float H = a2, K = -a2, ga = 0.0f, al0 = 0.0f, al1 = 0.0f, al2 = 0.0f, al3 = 0.0f;
+    const float lam = inv_mu * w_me;
+    // consensus state (warp 0): z, history ring c~_{t-r} (r = 0..3) and its norms
+    float z0 = m0, z1 = m1;
+    float h0[R], h1[R], nr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) h0[r] = h1[r] = nr[r] = 0.0f;
+    bool bad = false, ovf = false;
+
+    for (int t = 1; t <= T; ++t) {
+      // (1) D_k = <a~_k, c~_t>
+      float cv[J];
+      load_coords(cb, g, cv);
+      const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
+      const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
+      float2 dq[KP];
+#pragma unroll
+      for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < J; ++i)
+#pragma unroll
+        for (int m = 0; m < KP; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
+      const float Dk = group_rs8(dq, g);
+      // (2) scalar update of this lane's point
+      const float Gnn = gq2.x, nrR = gq2.y;
+      const float X = fmaf(al0, gq4.x, fmaf(al1, gq4.y, fmaf(al2, gq4.z, al3 * gq4.w)));
+      const float gp1 = ga + 1.0f;
+      const float HG = H + Gnn;
+      const float N = fmaf(2.0f, fmaf(-gp1, Dk, X), HG);
+      bad |= lam != 0.0f && !isfinite(N);
+      const float Nc = fmaxf(N, 0.0f);
+      const float s = lam != 0.0f ? fminf(1.0f, lam * rsq(Nc)) : 0.0f;
+      const float Bk = K + Dk;
+      const float ev = s * al3;
+      ovf |= ev * ev * nrR > kThr2 * Nc;
+      ovf |= lam != 0.0f && N < kCancel * HG;
+      H = fmaf(s, fmaf(s, Nc, -2.0f * Bk), a2);
+      K = fmaf(s, Bk, -a2);
+      ga = s * gp1;
+      al3 = s * al2;
+      al2 = s * al1;
+      al1 = s * al0;
+      al0 = s;
+      // (3) sum_k ga'_k a~_k per coordinate; history sums sum_k al'_r (onto lanes r = 0..3)
+      float2 gq[KP];
+      group_ag8(ga, gq, lane);
+      float v[J];
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(gq[m], A[m][i], acc);
+        v[i] = acc.x + acc.y;
+      }
+      float hs;
+      {
+        const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
+        const float x0 = (u2 ? al2 : al0) + __shfl_xor_sync(0xffffffffu, u2 ? al0 : al2, 2);
+        const float x1 = (u2 ? al3 : al1) + __shfl_xor_sync(0xffffffffu, u2 ? al1 : al3, 2);
+        hs = (u1 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, u1 ? x0 : x1, 1);
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+      }
+      fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
+      __syncthreads();
+      // (4) consensus (warp 0): z_t = P_C(z_{t-1} - g/n), c~_{t+1} = 2 z_t - z_{t-1} - m, and
+      // the Gram row of sweep t+1
+      if (warp == 0) {
+        const float2 S = rows_sum(red, lane);
+        float As[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) As[r] = __shfl_sync(0xffffffffu, S.y, 4 * r + 3);
+        float g0 = -S.x, g1 = -S.y;
+#pragma unroll
+        for (int r = R - 1; r >= 0; --r) {
+          g0 = fmaf(As[r], h0[r], g0);
+          g1 = fmaf(As[r], h1[r], g1);
+        }
+        const float zn0 = cv0 ? clamp_box(fmaf(-g0, inv_n, z0), box) : 0.0f;
+        const float zn1 = cv1 ? clamp_box(fmaf(-g1, inv_n, z1), box) : 0.0f;
+        bad |= !isfinite(zn0) || !isfinite(zn1);
+        const float c0 = cv0 ? (2.0f * zn0 - z0) - m0 : 0.0f;
+        const float c1 = cv1 ? (2.0f * zn1 - z1) - m1 : 0.0f;
+        z0 = zn0;
+        z1 = zn1;
+        float part[R + 1];
+#pragma unroll
+        for (int r = 0; r < R; ++r) part[r] = fmaf(h0[r], c0, h1[r] * c1);
+        part[R] = fmaf(c0, c0, c1 * c1);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int q = 0; q <= R; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
+        const float nr3 = nr[R - 1];
+#pragma unroll
+        for (int r = R - 1; r > 0; --r) {
+          h0[r] = h0[r - 1];
+          h1[r] = h1[r - 1];
+          nr[r] = nr[r - 1];
+        }
+        h0[0] = c0;
+        h1[0] = c1;
+        nr[0] = part[R];
+        reinterpret_cast<float2*>(cb)[lane] = make_float2(c0, c1);
+        if (lane == 0) {
+          reinterpret_cast<float4*>(gr)[0] = make_float4(part[0], part[1], part[2], part[3]);
+          reinterpret_cast<float2*>(gr)[2] = make_float2(part[R], nr3);
+        }
+      }
+      __syncthreads();
+    }
+
+    // ---- hand-off or outputs
+    if (__syncthreads_or(bad || ovf)) {
+      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      continue;
+    }
+    if (warp == 0) {
+      if (cv0) z_out[b * D + cj] = z0;
+      if (cv1) z_out[b * D + cj + 1] = z1;
+    }
+    if (iters_out != nullptr && tid == 0) iters_out[b] = T;
+    if (obj_out != nullptr) {
+      // em_cost(z) = sum_k w_k ||z - a_k|| (costs.hpp:13-20), z - a = (z - m) - a~
+      if (warp == 0) reinterpret_cast<float2*>(mb)[lane] = make_float2(z0 - m0, z1 - m1);
+      __syncthreads();
+      float zc[J];
+      load_coords(mb, g, zc);
+      float2 dq[KP];
+#pragma unroll
+      for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        const bool jr = 7 * g + i < D;
+#pragma unroll
+        for (int m = 0; m < KP; ++m) {
+          const float2 e = __fadd2_rn(f2(zc[i]), make_float2(-A[m][i].x, -A[m][i].y));
+          const float2 em = jr ? e : make_float2(0.0f, 0.0f);
+          dq[m] = __ffma2_rn(em, em, dq[m]);
+        }
+      }
+      const float dist2 = group_rs8(dq, g);
+      const float obj = block_sum(real_me ? w_me * sqrtf(dist2) : 0.0f, scal, warp, lane);
+      if (tid == 0) {
+        obj_out[b] = obj;
+        if (!isfinite(obj)) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      }
+    }
+  }
+  cp_wait_all();
+}
+
+bool admm_lr_supported(const AdmmLaunch& L) {
+  const char* force = std::getenv("NLEM_BATCHED");  // =fast forces the p-form kernel (A/B, tests)
+  if (force != nullptr && std::string(force) != "lr") return false;
+  return L.d == D && L.n >= 3 && L.n <= NCAP && L.res_mode != RES_FULL && L.tr_obj == nullptr &&
+         L.tr_res == nullptr && L.batch < (int64_t(1) << 31) &&
+         static_cast<int64_t>(L.n) * D < (int64_t(1) << 31) / 4;
+}
+
+cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cudaStream_t stream) {
+  auto kfn = admm_batched_lr;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM_BYTES));
+  if (e != cudaSuccess) return e;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
+  kfn<<<static_cast<unsigned>(grid), THREADS, SMEM_BYTES, stream>>>(
+      L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
+      L.iters_out, ho_list, ho_count);
+  return cudaGetLastError();
+}
+
+}  // namespace nlemk

@@ -340,12 +340,15 @@ __global__ void __launch_bounds__(C::THREADS, 1)
 admm_batched_fast(const float* __restrict__ points, const float* __restrict__ weights,
                   int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                   int T, int res_mode, float* z_out, float* obj_out, int* iters_out,
-                  FailureSlot* fail) {
+                  FailureSlot* fail, const int* list, const int* list_count) {
   extern __shared__ __align__(16) float smem[];
   FastCore<C> S;
   S.carve(smem);
   const size_t nd = static_cast<size_t>(n) * C::D;
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+  // list mode: the problems handed off by the low-rank kernel (kernels_batched_lr.cu)
+  const int64_t count = list != nullptr ? *list_count : batch;
+  for (int64_t ib = blockIdx.x; ib < count; ib += gridDim.x) {
+    const int64_t b = list != nullptr ? list[ib] : ib;
     const float* pts = points + b * nd;
     // a -> smem pairs (coalesced global reads along j)
     int neq = 0;
@@ -557,7 +560,8 @@ size_t fast_smem_bytes(bool tile) {
 }
 
 template <class C>
-cudaError_t launch_batched(const AdmmLaunch& L, cudaStream_t stream) {
+cudaError_t launch_batched(const AdmmLaunch& L, cudaStream_t stream, const int* list = nullptr,
+                           const int* list_count = nullptr) {
   const size_t smem = fast_smem_bytes<C>(false);
   auto kfn = admm_batched_fast<C>;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -569,7 +573,7 @@ cudaError_t launch_batched(const AdmmLaunch& L, cudaStream_t stream) {
       std::max<int64_t>(1, std::min<int64_t>(L.batch, int64_t(device_caps().sms) * std::max(per_sm, 1)));
   kfn<<<static_cast<unsigned>(grid), C::THREADS, smem, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.res_mode, L.z_out,
-      L.obj_out, L.iters_out, L.fail);
+      L.obj_out, L.iters_out, L.fail, list, list_count);
   return cudaGetLastError();
 }
 
@@ -602,7 +606,7 @@ cudaError_t launch_pixels(const NlemLaunch& L, cudaStream_t stream) {
 
 bool admm_fast_supported(const AdmmLaunch& L) {
   if (L.res_mode == RES_FULL || L.tr_obj != nullptr || L.tr_res != nullptr) return false;
-  if (L.n < 2) return false;
+  if (L.n < 3) return false;  // n <= 2: reference-form sweep (exact stops, use_ref_form)
   if (L.d == CfgD49::D && L.n <= CfgD49::NCAP) return true;
   if (L.d == CfgD25::D && L.n <= CfgD25::NCAP) return true;
   return false;
@@ -611,6 +615,12 @@ bool admm_fast_supported(const AdmmLaunch& L) {
 cudaError_t launch_admm_fast(const AdmmLaunch& L, cudaStream_t stream) {
   if (L.d == CfgD49::D) return launch_batched<CfgD49>(L, stream);
   return launch_batched<CfgD25>(L, stream);
+}
+
+cudaError_t launch_admm_fast_list(const AdmmLaunch& L, const int* list, const int* list_count,
+                                  cudaStream_t stream) {
+  if (L.d == CfgD49::D) return launch_batched<CfgD49>(L, stream, list, list_count);
+  return launch_batched<CfgD25>(L, stream, list, list_count);
 }
 
 bool nlem_fast_supported(const NlemLaunch& L) {

@@ -86,6 +86,14 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream);
 // shape is not covered (the caller then uses the generic kernel).
 bool admm_fast_supported(const AdmmLaunch& L);
 cudaError_t launch_admm_fast(const AdmmLaunch& L, cudaStream_t stream);
+// the same kernel over a device-side list of problem indices (count read on the device)
+cudaError_t launch_admm_fast_list(const AdmmLaunch& L, const int* list, const int* list_count,
+                                  cudaStream_t stream);
+// Low-rank (Gram-form) batched kernel for d = 49 (kernels_batched_lr.cu): problems it cannot
+// finish exactly (ring overflow, all points equal, non-finite values) are appended to ho_list
+// for launch_admm_fast_list.
+bool admm_lr_supported(const AdmmLaunch& L);
+cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cudaStream_t stream);
 bool nlem_seg2_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_seg2(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);

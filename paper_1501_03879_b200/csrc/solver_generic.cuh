@@ -91,13 +91,15 @@ __device__ float block_em_cost(const float* a, const float* w, int n, int d, con
   return tot;
 }
 
-// Problems at or below this dimension (and every n == 1 problem) run the reference
+// Problems at or below this dimension (and every n <= 2 problem) run the reference
 // form of the sweep verbatim: there the primal residual can hit exactly zero in
 // finitely many sweeps (1-D medians, single points: proj/tests/unit/test_solvers.cpp
-// :63-151), and only the reference's own arithmetic reproduces the exact stop.
+// :63-151; two points: the duals stay antisymmetric, the iterates stay on the line through
+// the points and x_1 == x_2 == z happens exactly, e.g. at sweep 3 for a random pair in d = 49,
+// in FP64 and FP32 alike), and only the reference's own arithmetic reproduces the exact stop.
 constexpr int kRefFormMaxDim = 16;
 
-__host__ __device__ inline bool use_ref_form(int n, int d) { return n == 1 || d <= kRefFormMaxDim; }
+__host__ __device__ inline bool use_ref_form(int n, int d) { return n <= 2 || d <= kRefFormMaxDim; }
 
 // floats of solver state per problem (p-form: p; reference form: x and y)
 __host__ __device__ inline size_t admm_state_floats(int n, int d) {
