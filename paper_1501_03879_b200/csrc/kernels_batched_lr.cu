@@ -32,6 +32,9 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#ifdef NLEM_BLR_STAMPS
+#include <cstdio>
+#endif
 
 #include "launch.h"
 
@@ -40,7 +43,9 @@ namespace nlemk {
 namespace blr {
 
 constexpr int D = 49, G = 8, J = 7, KP = G / 2;
-constexpr int WARPS = 14, THREADS = 32 * WARPS;
+constexpr int WARPS = 14;          // point warps
+constexpr int CW = WARPS;          // the consensus warp (no points)
+constexpr int NW = WARPS + 1, ALL = 32 * NW;
 constexpr int GPW = 32 / G, NG = GPW * WARPS, NCAP = NG * G;  // 56 groups, 448 points
 constexpr int R = 4;
 // Column layout of every per-coordinate row (partials, c~, m): lane g of a group owns
@@ -79,6 +84,19 @@ __device__ __forceinline__ float rsq(float x) {
   return y;
 }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
+// named barriers: the consensus warp arrives, the other warps wait (count = all threads)
+__device__ __forceinline__ void bar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(ALL) : "memory");
+}
+__device__ __forceinline__ void bar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(ALL) : "memory");
+}
+constexpr int BAR_C = 1, BAR_GRAM = 2;
+#ifdef NLEM_BLR_STAMPS
+#define BLR_STAMP(v) long long v = clock64()
+#else
+#define BLR_STAMP(v)
+#endif
 
 // element e of `src` lands at dst[shift(src) + e], shift = (src / 4) mod 4, so that global and
 // shared addresses agree mod 16 and the interior moves as 16-byte cp.async
@@ -89,7 +107,7 @@ __device__ __forceinline__ void stage_copy(float* dst, const float* src, int tot
   const int s0 = stage_shift(src);
   const int nch = (s0 + total + 3) >> 2;
   const float* base = src - s0;  // 16-byte aligned
-  for (int c = threadIdx.x; c < nch; c += THREADS) {
+  for (int c = threadIdx.x; c < nch; c += ALL) {
     const int e0 = 4 * c - s0;
     if (e0 >= 0 && e0 + 3 < total) {
       cp16(dst + 4 * c, base + 4 * c);
@@ -173,7 +191,7 @@ __device__ __forceinline__ float block_sum(float v, float* scal, int warp, int l
   __syncthreads();
   float t = 0.0f;
 #pragma unroll
-  for (int w = 0; w < WARPS; ++w) t += scal[w];
+  for (int w = 0; w < NW; ++w) t += scal[w];
   __syncthreads();
   return t;
 }
@@ -182,7 +200,7 @@ __device__ __forceinline__ float block_sum(float v, float* scal, int warp, int l
 
 using namespace blr;
 
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __launch_bounds__(ALL, 1)
 admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
                 int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                 int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
@@ -200,12 +218,13 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const int lane = tid & 31;
   const int g = lane & (G - 1);
   const int gid = warp * GPW + (lane >> 3);
-  float* const myrow = red + warp * RS;
+  const bool is_pts = warp < WARPS;
+  float* const myrow = red + (is_pts ? warp : 0) * RS;
   // point of slot q of this lane's group: pair m = q / 2 is point pair m * NG + gid
   auto point_of = [&](int q) { return 2 * ((q >> 1) * NG + gid) + (q & 1); };
   const int k_me = point_of(g);
-  const bool real_me = k_me < n;
-  // consensus (warp 0): lane l finishes columns 2l, 2l+1 = coordinates cj, cj + 1
+  const bool real_me = is_pts && k_me < n;
+  // consensus (warp CW): lane l finishes columns 2l, 2l+1 = coordinates cj, cj + 1
   const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
   const int cj = 7 * cgrp + cidx;
   const bool cv0 = cgrp < 7, cv1 = cgrp < 7 && (lane & 3) != 3;
@@ -230,21 +249,22 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     float2 A[KP][J];
     float2 wq[KP];
     int neq = 0;
+    const bool greal = is_pts && g < 7;  // lane g = 7 of a group: padding coordinates 49..55
+    float r0[J];
+#pragma unroll
+    for (int i = 0; i < J; ++i) r0[i] = greal ? st[7 * g + i] : 0.0f;
 #pragma unroll
     for (int m = 0; m < KP; ++m) {
       const int k0 = 2 * (m * NG + gid), k1 = k0 + 1;
-      wq[m] = make_float2(k0 < n ? wv[k0] : 0.0f, k1 < n ? wv[k1] : 0.0f);
+      const bool h0 = greal && k0 < n, h1 = greal && k1 < n;
+      wq[m] = make_float2(is_pts && k0 < n ? wv[k0] : 0.0f, is_pts && k1 < n ? wv[k1] : 0.0f);
+      const float* p0 = st + k0 * D + 7 * g;
+      const float* p1 = st + k1 * D + 7 * g;
 #pragma unroll
       for (int i = 0; i < J; ++i) {
-        const int j = 7 * g + i;
-        float v0 = 0.0f, v1 = 0.0f;
-        if (j < D) {
-          const float r0 = st[j];
-          if (k0 < n) v0 = st[k0 * D + j];
-          if (k1 < n) v1 = st[k1 * D + j];
-          neq |= (k0 < n && v0 != r0) | (k1 < n && v1 != r0);
-        }
-        A[m][i] = make_float2(v0, v1);
+        const float v0 = h0 ? p0[i] : r0[i], v1 = h1 ? p1[i] : r0[i];
+        neq |= (v0 != r0[i]) | (v1 != r0[i]);
+        A[m][i] = make_float2(h0 ? v0 : 0.0f, h1 ? v1 : 0.0f);
       }
     }
     const float w_me = real_me ? wv[k_me] : 0.0f;
@@ -261,12 +281,13 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     }
 
     // ---- z_0 = m: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
-    float m0 = 0.0f, m1 = 0.0f;  // warp 0: m at coordinates cj, cj + 1
+    float m0 = 0.0f, m1 = 0.0f;  // consensus warp: m at coordinates cj, cj + 1
     if (z_init == nullptr) {
       const float W = block_sum(w_me, scal, warp, lane);
       float2 coef[KP];
+      const float rW = 1.0f / W;
 #pragma unroll
-      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x / W, wq[m].y / W);
+      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x * rW, wq[m].y * rW);
       float v[J];
 #pragma unroll
       for (int i = 0; i < J; ++i) {
@@ -275,10 +296,10 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         for (int m = 0; m < KP; ++m) acc = __ffma2_rn(coef[m], A[m][i], acc);
         v[i] = acc.x + acc.y;
       }
-      fold_store(v, 0.0f, myrow, lane);
+      if (is_pts) fold_store(v, 0.0f, myrow, lane);
       __syncthreads();
     }
-    if (warp == 0) {
+    if (warp == CW) {
       if (z_init != nullptr) {
         m0 = cv0 ? z_init[b * D + cj] : 0.0f;
         m1 = cv1 ? z_init[b * D + cj + 1] : 0.0f;
@@ -301,13 +322,12 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       for (int m = 0; m < KP; ++m) nq[m] = make_float2(0.0f, 0.0f);
 #pragma unroll
       for (int i = 0; i < J; ++i) {
-        const int j = 7 * g + i;
 #pragma unroll
         for (int m = 0; m < KP; ++m) {
           const int k0 = 2 * (m * NG + gid);
           const float2 a = A[m][i];
-          A[m][i] = make_float2(j < D && k0 < n ? a.x - mc[i] : 0.0f,
-                                j < D && k0 + 1 < n ? a.y - mc[i] : 0.0f);
+          A[m][i] = make_float2(greal && k0 < n ? a.x - mc[i] : 0.0f,
+                                greal && k0 + 1 < n ? a.y - mc[i] : 0.0f);
           nq[m] = __ffma2_rn(A[m][i], A[m][i], nq[m]);
         }
       }
@@ -316,19 +336,26 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     // per-point state (own slot): p_1 = z_0 - a = -a~ (u = 0, admm.hpp:41)
     float H = a2, K = -a2, ga = 0.0f, al0 = 0.0f, al1 = 0.0f, al2 = 0.0f, al3 = 0.0f;
     const float lam = inv_mu * w_me;
-    // consensus state (warp 0): z, history ring c~_{t-r} (r = 0..3) and its norms
+    // consensus state (warp CW): z, history ring c~_{t-r} (r = 0..3) and its norms
     float z0 = m0, z1 = m1;
     float h0[R], h1[R], nr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) h0[r] = h1[r] = nr[r] = 0.0f;
     bool bad = false, ovf = false;
+#ifdef NLEM_BLR_STAMPS
+    long long st_wc = 0, st_wg = 0, st_a = 0, st_b1 = 0, st_cons = 0;
+#endif
 
     for (int t = 1; t <= T; ++t) {
+     if (is_pts) {
       // (1) D_k = <a~_k, c~_t>
+      // c~_t is published by the consensus warp before its Gram row (named barriers): the dot
+      // products overlap the Gram reduction
+      BLR_STAMP(s0);
+      if (t > 1) bar_sync(BAR_C);
+      BLR_STAMP(s1);
       float cv[J];
       load_coords(cb, g, cv);
-      const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
-      const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
       float2 dq[KP];
 #pragma unroll
       for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
@@ -338,6 +365,11 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         for (int m = 0; m < KP; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
       const float Dk = group_rs8(dq, g);
       // (2) scalar update of this lane's point
+      BLR_STAMP(s2);
+      if (t > 1) bar_sync(BAR_GRAM);
+      BLR_STAMP(s3);
+      const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
+      const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
       const float Gnn = gq2.x, nrR = gq2.y;
       const float X = fmaf(al0, gq4.x, fmaf(al1, gq4.y, fmaf(al2, gq4.z, al3 * gq4.w)));
       const float gp1 = ga + 1.0f;
@@ -378,10 +410,21 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
       }
       fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
+      BLR_STAMP(s4);
       __syncthreads();
-      // (4) consensus (warp 0): z_t = P_C(z_{t-1} - g/n), c~_{t+1} = 2 z_t - z_{t-1} - m, and
+      BLR_STAMP(s5);
+#ifdef NLEM_BLR_STAMPS
+      st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
+#endif
+     } else {
+      BLR_STAMP(s4);
+      __syncthreads();
+      BLR_STAMP(s5);
+#ifdef NLEM_BLR_STAMPS
+      st_b1 += s5 - s4;
+#endif
+      // (4) consensus (warp CW): z_t = P_C(z_{t-1} - g/n), c~_{t+1} = 2 z_t - z_{t-1} - m, and
       // the Gram row of sweep t+1
-      if (warp == 0) {
         const float2 S = rows_sum(red, lane);
         float As[R];
 #pragma unroll
@@ -399,6 +442,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         const float c1 = cv1 ? (2.0f * zn1 - z1) - m1 : 0.0f;
         z0 = zn0;
         z1 = zn1;
+        reinterpret_cast<float2*>(cb)[lane] = make_float2(c0, c1);
+        __syncwarp();
+        if (t < T) bar_arrive(BAR_C);
         float part[R + 1];
 #pragma unroll
         for (int r = 0; r < R; ++r) part[r] = fmaf(h0[r], c0, h1[r] * c1);
@@ -417,28 +463,37 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         h0[0] = c0;
         h1[0] = c1;
         nr[0] = part[R];
-        reinterpret_cast<float2*>(cb)[lane] = make_float2(c0, c1);
         if (lane == 0) {
           reinterpret_cast<float4*>(gr)[0] = make_float4(part[0], part[1], part[2], part[3]);
           reinterpret_cast<float2*>(gr)[2] = make_float2(part[R], nr3);
         }
-      }
-      __syncthreads();
+        __syncwarp();
+        if (t < T) bar_arrive(BAR_GRAM);
+#ifdef NLEM_BLR_STAMPS
+        BLR_STAMP(s6);
+        st_cons += s6 - s5;
+#endif
+     }
     }
 
+#ifdef NLEM_BLR_STAMPS
+    if (blockIdx.x == 0 && b < 3 * gridDim.x && (tid == 0 || tid == 32 || tid == CW * 32))
+      printf("blr stamps warp %d T %d: wait_c %lld wait_gram %lld phaseA %lld wait_b1 %lld cons %lld (per sweep)\n",
+             warp, T, st_wc / T, st_wg / T, st_a / T, st_b1 / T, st_cons / T);
+#endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       continue;
     }
-    if (warp == 0) {
+    if (warp == CW) {
       if (cv0) z_out[b * D + cj] = z0;
       if (cv1) z_out[b * D + cj + 1] = z1;
     }
     if (iters_out != nullptr && tid == 0) iters_out[b] = T;
     if (obj_out != nullptr) {
       // em_cost(z) = sum_k w_k ||z - a_k|| (costs.hpp:13-20), z - a = (z - m) - a~
-      if (warp == 0) reinterpret_cast<float2*>(mb)[lane] = make_float2(z0 - m0, z1 - m1);
+      if (warp == CW) reinterpret_cast<float2*>(mb)[lane] = make_float2(z0 - m0, z1 - m1);
       __syncthreads();
       float zc[J];
       load_coords(mb, g, zc);
@@ -480,7 +535,7 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cud
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
-  kfn<<<static_cast<unsigned>(grid), THREADS, SMEM_BYTES, stream>>>(
+  kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
       L.iters_out, ho_list, ho_count);
   return cudaGetLastError();
