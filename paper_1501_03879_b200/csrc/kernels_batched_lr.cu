@@ -62,7 +62,8 @@ constexpr int SM_CB = SM_RED + WARPS * RS;       // [RS] c~ of the coming sweep
 constexpr int SM_MB = SM_CB + RS;                // [RS] m (centring), then z~ for the cost
 constexpr int SM_GR = SM_MB + RS;                // [8] Gram row: G_0..G_3, ||c~||^2, ||c~_{t-4}||^2
 constexpr int SM_SCAL = SM_GR + 8;               // [32] block-sum scratch
-constexpr int SM_TOTAL = SM_SCAL + 32;
+constexpr int SM_PIN = SM_SCAL + 32;             // [ALL] barrier-ordering scratch
+constexpr int SM_TOTAL = SM_PIN + ALL;
 constexpr size_t SMEM_BYTES = size_t(SM_TOTAL) * sizeof(float);
 static_assert(NCAP >= 441, "config-1 capacity");
 static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_GR % 4 == 0, "alignment");
@@ -91,6 +92,9 @@ __device__ __forceinline__ void bar_sync(int id) {
 __device__ __forceinline__ void bar_arrive(int id) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(ALL) : "memory");
 }
+// Barriers only order memory operations: ptxas freely moves register arithmetic and shuffles
+// across them.  To keep work on the intended side, a value is stored to / reloaded from shared
+// memory at the barrier (a store cannot sink below it, a load cannot rise above it).
 constexpr int BAR_C = 1, BAR_GRAM = 2;
 #ifdef NLEM_BLR_STAMPS
 #define BLR_STAMP(v) long long v = clock64()
@@ -213,6 +217,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   float* const mb = smem + SM_MB;
   float* const gr = smem + SM_GR;
   float* const scal = smem + SM_SCAL;
+  float* const pin = smem + SM_PIN;
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int lane = tid & 31;
@@ -343,7 +348,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     for (int r = 0; r < R; ++r) h0[r] = h1[r] = nr[r] = 0.0f;
     bool bad = false, ovf = false;
 #ifdef NLEM_BLR_STAMPS
-    long long st_wc = 0, st_wg = 0, st_a = 0, st_b1 = 0, st_cons = 0;
+    long long st_wc = 0, st_wg = 0, st_a = 0, st_b1 = 0, st_cons = 0, st_q[6] = {0, 0, 0, 0, 0, 0};
 #endif
 
     for (int t = 1; t <= T; ++t) {
@@ -363,10 +368,15 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       for (int i = 0; i < J; ++i)
 #pragma unroll
         for (int m = 0; m < KP; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
+      BLR_STAMP(q0);
       const float Dk = group_rs8(dq, g);
+      BLR_STAMP(q1);
       // (2) scalar update of this lane's point
       BLR_STAMP(s2);
-      if (t > 1) bar_sync(BAR_GRAM);
+      if (t > 1) {
+        pin[tid] = Dk;  // the dot products and their reduction run before the wait
+        bar_sync(BAR_GRAM);
+      }
       BLR_STAMP(s3);
       const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
       const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
@@ -390,8 +400,10 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       al1 = s * al0;
       al0 = s;
       // (3) sum_k ga'_k a~_k per coordinate; history sums sum_k al'_r (onto lanes r = 0..3)
+      BLR_STAMP(q2);
       float2 gq[KP];
       group_ag8(ga, gq, lane);
+      BLR_STAMP(q3);
       float v[J];
 #pragma unroll
       for (int i = 0; i < J; ++i) {
@@ -400,6 +412,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         for (int m = 0; m < KP; ++m) acc = __ffma2_rn(gq[m], A[m][i], acc);
         v[i] = acc.x + acc.y;
       }
+      BLR_STAMP(q4);
       float hs;
       {
         const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
@@ -415,6 +428,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       BLR_STAMP(s5);
 #ifdef NLEM_BLR_STAMPS
       st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
+      st_q[0] += q0 - s1; st_q[1] += q1 - q0; st_q[2] += q2 - s3; st_q[3] += q3 - q2; st_q[4] += q4 - q3; st_q[5] += s4 - q4;
 #endif
      } else {
       BLR_STAMP(s4);
@@ -445,10 +459,12 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         reinterpret_cast<float2*>(cb)[lane] = make_float2(c0, c1);
         __syncwarp();
         if (t < T) bar_arrive(BAR_C);
+        const float2 cg = reinterpret_cast<const float2*>(cb)[lane];  // Gram after the arrive
+        const float c0g = cg.x, c1g = cg.y;
         float part[R + 1];
 #pragma unroll
-        for (int r = 0; r < R; ++r) part[r] = fmaf(h0[r], c0, h1[r] * c1);
-        part[R] = fmaf(c0, c0, c1 * c1);
+        for (int r = 0; r < R; ++r) part[r] = fmaf(h0[r], c0g, h1[r] * c1g);
+        part[R] = fmaf(c0g, c0g, c1g * c1g);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
@@ -480,6 +496,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     if (blockIdx.x == 0 && b < 3 * gridDim.x && (tid == 0 || tid == 32 || tid == CW * 32))
       printf("blr stamps warp %d T %d: wait_c %lld wait_gram %lld phaseA %lld wait_b1 %lld cons %lld (per sweep)\n",
              warp, T, st_wc / T, st_wg / T, st_a / T, st_b1 / T, st_cons / T);
+    if (blockIdx.x == 0 && b < 3 * gridDim.x && tid == 32)
+      printf("blr phaseA: dot %lld rs8 %lld scalar %lld ag8 %lld wsum %lld fold+hs+sts %lld\n", st_q[0] / T,
+             st_q[1] / T, st_q[2] / T, st_q[3] / T, st_q[4] / T, st_q[5] / T);
 #endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
