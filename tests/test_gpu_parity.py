@@ -440,3 +440,21 @@ def test_lr_kernel_matches_tile_kernel(nb, tmp_path):
     kw = dict(search=21, patch=7, h=1e30, sigma=10.0, solver="admm", solver_iters=4, mu=1.0,
               unbounded=True)
     assert _run_forced_kernel("lr", img, kw, tmp_path) == _run_forced_kernel("tile", img, kw, tmp_path)
+
+
+@pytest.mark.parametrize("mu,iters", [(1.0, 10), (0.05, 20)])
+def test_lr_noiseless_piecewise_constant(nb, oracle, tmp_path, mu, iters):
+    """Noise-free piecewise-constant image (sigma = 0): near edges many window points coincide
+    with the consensus while their centred norms ||a - a_self|| are large, where the Gram
+    expansion of ||p||^2 could cancel; flat footprints take the exact stop.  The low-rank kernel
+    (with its ring hand-off at the smaller mu) matches the oracle on every frame."""
+    from paper_1501_03879_b200 import synth
+
+    clean, _ = synth.noisy_image(40, 44, 10, 6, 0.0)
+    kw = dict(search=21, patch=7, h=synth.reference_h(20.0, 49), solver="admm", solver_iters=iters,
+              mu=mu, init_mode="nlm")
+    lr = _run_forced_kernel("lr", clean, kw, tmp_path)
+    g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(20.0, 49), iters=iters,
+                        mu=mu)
+    _, fo = oracle.nlem_denoise(clean.astype(np.float64), o, snapshots=True)
+    assert np.abs(lr - fo).max() <= TOL
