@@ -458,3 +458,34 @@ def test_lr_noiseless_piecewise_constant(nb, oracle, tmp_path, mu, iters):
                         mu=mu)
     _, fo = oracle.nlem_denoise(clean.astype(np.float64), o, snapshots=True)
     assert np.abs(lr - fo).max() <= TOL
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 9), (7, 3), (13, 30), (30, 13), (22, 23)])
+def test_ragged_and_tiny_images(nb, oracle, tmp_path, shape):
+    """Images smaller than the search window in one or both directions (the window is clipped
+    to n = 1 .. 441 points, the mirror reflection of patch.cpp:9-16 wraps several times, n = 1
+    mirrors to index 0), through every kernel family: low-rank (k=7, S=21), tile (k=5, S=11,
+    and the hand-off target for k=7), generic (k=3, S=5), each vs the oracle on every frame."""
+    from paper_1501_03879_b200 import synth
+
+    rng = np.random.default_rng(shape[0] * 100 + shape[1])
+    img = (rng.uniform(0, 255, shape) + rng.normal(0, 20, shape)).astype(np.float32)
+    for kernel, k, S in (("lr", 7, 21), ("tile", 7, 21), ("tile", 5, 11), ("generic", 3, 5)):
+        h = synth.reference_h(20.0, k * k)
+        kw = dict(search=S, patch=k, h=h, solver="admm", solver_iters=6, mu=1.0, init_mode="nlm")
+        out = _run_forced_kernel(kernel, img, kw, tmp_path)
+        g, o = _params_pair(nb, oracle, search=S, patch=k, h=h, iters=6)
+        _, fo = oracle.nlem_denoise(img.astype(np.float64), o, snapshots=True)
+        assert out.shape == fo.shape, (kernel, k)
+        assert np.abs(out - fo).max() <= TOL, (kernel, k, S, shape)
+
+
+def test_empty_and_nonfinite_images_rejected(nb):
+    """validate_image (image.hpp:14-17): empty and non-finite images are invalid arguments."""
+    p = nb.NlemParams(search=21, patch=7, h=1400.0, solver_iters=2, mu=1.0)
+    with pytest.raises(nb.InvalidArgument, match="image must be non-empty"):
+        nb.nlem_denoise(np.zeros((0, 5), np.float32), p)
+    bad = np.zeros((9, 9), np.float32)
+    bad[4, 4] = np.nan
+    with pytest.raises(nb.InvalidArgument, match="image intensities must be finite"):
+        nb.nlem_denoise(bad, p)
