@@ -183,6 +183,18 @@ nlem_status nlem_denoise_host(const float* noisy, int64_t rows, int64_t cols,
                               const nlem_params* params, float* out, float* frames,
                               nlem_failure* failure, int32_t device);
 
+/* Whole-image NLEM from host buffers over several GPUs of one node: the image is cut into
+ * ndev contiguous row bands, band i runs nlem_denoise_rows_host on devices[i]
+ * from its own host thread with its own 13-row halo (S/2 + k/2), and no collective runs.  The
+ * result (and frames, [solver_iters][rows][cols] host, or NULL) is bitwise identical to the
+ * single-device call; a NumericFailure reports the lowest failing pixel over all bands, as
+ * the single call does.  devices may repeat (several bands per GPU).  This replaces the
+ * reference's internal thread pool (NlemParams::threads, proj/src/nlem.cpp:68-90 with
+ * parallel.hpp:20-55) by a device pool. */
+nlem_status nlem_denoise_multi_host(const float* noisy, int64_t rows, int64_t cols,
+                                    const nlem_params* params, float* out, float* frames,
+                                    const int32_t* devices, int32_t ndev, nlem_failure* failure);
+
 /* Classical non-local means (proj/src/nlm.cpp:31-51). */
 nlem_status nlm_denoise(const float* noisy, int64_t rows, int64_t cols, const nlem_params* params,
                         float* out, nlem_failure* failure, void* stream);

@@ -216,6 +216,20 @@ inline Image nlem_denoise(const Image& noisy, const NlemParams& params, int devi
   return out;
 }
 
+// proj/src/nlem.cpp:68-90 over a pool of devices (the reference's NlemParams::threads pool,
+// parallel.hpp:20-55, becomes one row band per device; bitwise equal to one device)
+inline Image nlem_denoise(const Image& noisy, const NlemParams& params,
+                          const std::vector<int32_t>& devices) {
+  Image out(noisy.rows(), noisy.cols());
+  const nlem_params p = params.c();
+  nlem_failure f;
+  detail::raise(nlem_denoise_multi_host(noisy.data(), noisy.rows(), noisy.cols(), &p, out.data(),
+                                        nullptr, devices.data(),
+                                        static_cast<int32_t>(devices.size()), &f),
+                f);
+  return out;
+}
+
 // proj/src/nlem.cpp:92-128
 inline std::vector<Image> nlem_denoise_snapshots(const Image& noisy, const NlemParams& params,
                                                  int device = 0) {

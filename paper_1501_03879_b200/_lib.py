@@ -51,7 +51,8 @@ EXPORTS = [
     "nlem_version", "nlem_status_string", "nlem_validate_params", "nlem_default_init_mode",
     "nlem_admm_batched", "nlem_admm_batched_host", "nlem_irls_batched",
     "nlem_irls_batched_host", "nlem_denoise",
-    "nlem_denoise_rows", "nlem_denoise_rows_host", "nlem_denoise_host", "nlm_denoise", "nlem_band_halo",
+    "nlem_denoise_rows", "nlem_denoise_rows_host", "nlem_denoise_host", "nlem_denoise_multi_host",
+    "nlm_denoise", "nlem_band_halo",
     "nlem_add_gaussian_noise", "nlem_synth_clean_image", "nlem_synth_noisy_image",
     "nlem_synth_point_sets", "nlem_frames_psnr", "nlem_optimality_residual_batched",
 ]
@@ -100,6 +101,8 @@ def load(build_if_missing: bool = True):
                                          C.POINTER(Failure), C.c_int32]
     L.nlem_denoise_host.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(ParamsC), vp, vp,
                                     C.POINTER(Failure), C.c_int32]
+    L.nlem_denoise_multi_host.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(ParamsC), vp, vp,
+                                          C.POINTER(C.c_int32), C.c_int32, C.POINTER(Failure)]
     L.nlm_denoise.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(ParamsC), vp,
                               C.POINTER(Failure), vp]
     L.nlem_frames_psnr.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, C.POINTER(Failure), vp]

@@ -357,6 +357,23 @@ def nlem_denoise_host(noisy: np.ndarray, params: NlemParams, out: np.ndarray | N
     return out
 
 
+def nlem_denoise_multi_host(noisy: np.ndarray, params: NlemParams, devices, frames: bool = False):
+    """Whole image over several devices (nlem_denoise_multi_host): one row band per entry of
+    `devices` (entries may repeat), one host thread per band, no collective.  Returns out, or
+    (out, frames [solver_iters][rows][cols]) with frames=True; bitwise equal to one device."""
+    noisy = np.ascontiguousarray(noisy, dtype=np.float32)
+    out = np.empty_like(noisy)
+    fr = np.empty((params.solver_iters,) + noisy.shape, np.float32) if frames else None
+    devs = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+    f = L.Failure()
+    st = L.load().nlem_denoise_multi_host(noisy.ctypes.data, noisy.shape[0], noisy.shape[1],
+                                          C.byref(params.c()), out.ctypes.data,
+                                          fr.ctypes.data if frames else None, devs, len(devices),
+                                          C.byref(f))
+    _raise(st, f)
+    return (out, fr) if frames else out
+
+
 def nlem_denoise_rows_host(noisy_rows: np.ndarray, in_row0: int, rows: int, cols: int,
                            out_row0: int, out_rows: int, params: NlemParams,
                            out: np.ndarray | None = None, device: int = 0) -> np.ndarray:

@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu",
               "kernels_nlem_seg2.cu", "kernels_nlem_lr.cu", "kernels_batched_lr.cu",
               "kernels_aux.cu"]
-CXX_SOURCES = ["synth.cpp"]
+CXX_SOURCES = ["synth.cpp", "multi_host.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++20", "--expt-relaxed-constexpr",

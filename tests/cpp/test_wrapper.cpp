@@ -101,6 +101,17 @@ int main() {
     }
     CHECK(caught);
   }
+  {  // device pool (nlem_denoise_multi_host): 3 bands on device 0 == the single call, bitwise
+    Image img(23, 17);
+    for (int r = 0; r < 23; ++r)
+      for (int c = 0; c < 17; ++c) img(r, c) = static_cast<float>((r * 37 + c * 11) % 256);
+    Image one = nlem_denoise(img, params);
+    Image three = nlem_denoise(img, params, std::vector<int32_t>{0, 0, 0});
+    bool same = true;
+    for (int r = 0; r < 23; ++r)
+      for (int c = 0; c < 17; ++c) same &= one(r, c) == three(r, c);
+    CHECK(same);
+  }
   CHECK(default_init_mode(60.5) == PatchInit::NlmPatch);
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);
   return failures ? 1 : 0;

@@ -489,3 +489,29 @@ def test_empty_and_nonfinite_images_rejected(nb):
     bad[4, 4] = np.nan
     with pytest.raises(nb.InvalidArgument, match="image intensities must be finite"):
         nb.nlem_denoise(bad, p)
+
+
+def test_device_pool_matches_single_device(nb):
+    """nlem_denoise_multi_host: 1, 2, 3 and 5 row bands (all on device 0 here; one host thread
+    each) give bitwise the single-device output and frames, and a numeric failure reports the
+    same lowest failing pixel as the single call (test_denoise.cpp:323-338 style input)."""
+    from paper_1501_03879_b200 import synth
+
+    _, noisy = synth.noisy_image(61, 47, 8, 5, 20.0)
+    p = nb.NlemParams(search=21, patch=7, h=synth.reference_h(20.0, 49), solver_iters=5, mu=1.0,
+                      init_mode="nlm")
+    one, fr1 = nb.nlem_denoise_multi_host(noisy, p, [0], frames=True)
+    assert np.array_equal(one, nb.nlem_denoise_host(noisy, p))
+    for devs in ([0, 0], [0, 0, 0], [0] * 5):
+        out, fr = nb.nlem_denoise_multi_host(noisy, p, devs, frames=True)
+        assert np.array_equal(out, one) and np.array_equal(fr, fr1), devs
+    img = np.zeros((30, 30), np.float32)
+    img[12:18, 12:18] = np.where(np.add.outer(np.arange(6), np.arange(6)) % 2 == 0, 0.0, 3e19)
+    q = nb.NlemParams(search=21, patch=7, h=1e30, sigma=10.0, solver_iters=4, mu=1.0,
+                      range=nb.BoxConstraint.unconstrained())
+    msgs = []
+    for devs in ([0], [0, 0, 0]):
+        with pytest.raises(nb.NumericFailure) as e:
+            nb.nlem_denoise_multi_host(img, q, devs)
+        msgs.append((str(e.value), e.value.iteration, e.value.index))
+    assert msgs[0] == msgs[1]
