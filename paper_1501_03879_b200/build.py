@@ -48,7 +48,8 @@ def _stale() -> bool:
 # experimental build variants (A/B and debug only): "_"-separated tokens -> defines
 _VARIANT_TOKENS = {
     "prof": "-DNLEM_PHASE_PROFILE",  # clock64 phase stamps (nlem_debug_phase_times)
-    "blrst": "-DNLEM_BLR_STAMPS",    # batched low-rank kernel: per-phase clock64 sums (printf)
+    "blrst": "-DNLEM_BLR_STAMPS",
+    "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-pixel phase clock64 sums (printf)    # batched low-rank kernel: per-phase clock64 sums (printf)
     "cl2": "-DNLEM_TILE_CL=2",       # 2-CTA cluster tile kernel
     "xw0": "-DNLEM_TILE_XW=0",       # consensus spread over the point warps
     "xw1": "-DNLEM_TILE_XW=1",       # dedicated consensus warp

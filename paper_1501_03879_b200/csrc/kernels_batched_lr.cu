@@ -237,6 +237,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const float inv_n = 1.0f / static_cast<float>(n);
   const int nd = n * D;
 
+#ifdef NLEM_BLR_STAMPS
+  long long su_wait = 0, su_load = 0, su_pref = 0, su_init = 0, su_sw = 0, su_epi = 0, su_n = 0;
+#endif
   int64_t b = blockIdx.x;
   if (b < batch) {
     stage_copy(stage, points + b * nd, nd);
@@ -245,8 +248,14 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   cp_commit();
 
   for (; b < batch; b += gridDim.x) {
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t0 = clock64();
+#endif
     cp_wait_all();
     __syncthreads();
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t1 = clock64(); su_wait += su_t1 - su_t0;
+#endif
     // ---- this problem's points (raw) into registers, weights, all-equal test
     const float* const src = points + b * nd;
     const float* const st = stage + stage_shift(src);
@@ -274,6 +283,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     }
     const float w_me = real_me ? wv[k_me] : 0.0f;
     const bool static_eq = !__syncthreads_or(neq);  // every thread is done with the stage
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t2 = clock64(); su_load += su_t2 - su_t1;
+#endif
     const int64_t bn = b + gridDim.x;
     if (bn < batch) {
       stage_copy(stage, points + bn * nd, nd);
@@ -285,6 +297,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       continue;
     }
 
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t3 = clock64(); su_pref += su_t3 - su_t2;
+#endif
     // ---- z_0 = m: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
     float m0 = 0.0f, m1 = 0.0f;  // consensus warp: m at coordinates cj, cj + 1
     if (z_init == nullptr) {
@@ -351,6 +366,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     long long st_wc = 0, st_wg = 0, st_a = 0, st_b1 = 0, st_cons = 0, st_q[6] = {0, 0, 0, 0, 0, 0};
 #endif
 
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t4 = clock64(); su_init += su_t4 - su_t3;
+#endif
     for (int t = 1; t <= T; ++t) {
      if (is_pts) {
       // (1) D_k = <a~_k, c~_t>
@@ -500,6 +518,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       printf("blr phaseA: dot %lld rs8 %lld scalar %lld ag8 %lld wsum %lld fold+hs+sts %lld\n", st_q[0] / T,
              st_q[1] / T, st_q[2] / T, st_q[3] / T, st_q[4] / T, st_q[5] / T);
 #endif
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t5 = clock64(); su_sw += su_t5 - su_t4;
+#endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
@@ -536,7 +557,16 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         if (!isfinite(obj)) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       }
     }
+#ifdef NLEM_BLR_STAMPS
+    { const long long e_ = clock64(); su_epi += e_ - su_t5; ++su_n; }
+#endif
   }
+#ifdef NLEM_BLR_STAMPS
+  if (blockIdx.x < 2 && (tid == 0 || tid == CW * 32) && su_n)
+    printf("blr setup blk %d warp %d: problems %lld wait %lld load %lld prefetch %lld init %lld sweeps %lld epilogue %lld\n",
+           blockIdx.x, warp, su_n, su_wait / su_n, su_load / su_n, su_pref / su_n, su_init / su_n,
+           su_sw / su_n, su_epi / su_n);
+#endif
   cp_wait_all();
 }
 

@@ -37,6 +37,7 @@
 //    are finished by their owner lanes, which keep z, m and the c~ history in registers; the
 //    Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -421,11 +422,20 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   }
   if (pix < plane) issue_tile(pix, 0);
 
+#ifdef NLEM_LR_STAMPS
+  long long st_t0 = 0, st_t1 = 0, st_t2 = 0, st_t3 = 0, st_wait = 0, st_setup = 0, st_sw = 0, st_epi = 0, st_n = 0;
+#endif
   while (pix < plane) {
     int nxt = 0;
     if (lane == 0) nxt = atomicAdd(work_counter, 1) + total_warps;
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
+#ifdef NLEM_LR_STAMPS
+    st_t0 = clock64();
+#endif
     cpa_wait();
+#ifdef NLEM_LR_STAMPS
+    st_t1 = clock64(); st_wait += st_t1 - st_t0;
+#endif
     __syncwarp();
     const float* const T = W;
 
@@ -676,6 +686,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       if (ifail_iter < 0) iters = stop_at > 0 ? stop_at : P.iters;
     } else {
     publish();
+#ifdef NLEM_LR_STAMPS
+    st_t2 = clock64(); st_setup += st_t2 - st_t1;
+#endif
     for (int t = 1; t <= P.iters; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
@@ -829,6 +842,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     }
     }  // ADMM
     tm_wait_st();
+#ifdef NLEM_LR_STAMPS
+    st_t3 = clock64(); st_sw += st_t3 - st_t2;
+#endif
     const bool any_ovf = __any_sync(0xffffffffu, ovf);
     if (any_ovf) {
       // a dropped history term would have been significant: the exact p-form kernel redoes it
@@ -851,7 +867,15 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     __syncwarp();  // every lane is done with the tile before the next one streams in
     if (nxt < plane) issue_tile(nxt, 0);
     pix = nxt;
+#ifdef NLEM_LR_STAMPS
+    { const long long e_ = clock64(); st_epi += e_ - st_t3; ++st_n; }
+#endif
   }
+#ifdef NLEM_LR_STAMPS
+  if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 7) && st_n)
+    printf("lr stamps blk %d warp %d: pixels %lld tile_wait %lld setup %lld sweeps %lld epilogue %lld (cycles/pixel)\n",
+           blockIdx.x, warp, st_n, st_wait / st_n, st_setup / st_n, st_sw / st_n, st_epi / st_n);
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
