@@ -424,6 +424,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 
 #ifdef NLEM_LR_STAMPS
   long long st_t0 = 0, st_t1 = 0, st_t2 = 0, st_t3 = 0, st_wait = 0, st_setup = 0, st_sw = 0, st_epi = 0, st_n = 0;
+  long long st_p[4] = {0, 0, 0, 0};
 #endif
   while (pix < plane) {
     int nxt = 0;
@@ -446,15 +447,32 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     const int gc1 = cols - 1 - c < HS ? HS + (cols - 1 - c) : SW - 1;
     const float inv_n = 1.0f / static_cast<float>((gr1 - gr0 + 1) * (gc1 - gc0 + 1));
 
+#ifdef NLEM_LR_STAMPS
+    long long st_q = clock64();
+#endif
     // ---- footprint constancy (exact-stop candidate, admm.hpp:77 with tol 0)
     const float a0 = tile_at(T, gr0, gc0);
     bool neq = false;
     if (lane >= gc0 && lane <= gc1 + KS - 1) {
+      // column `lane` of the footprint rows [gr0, gr1 + 6]: each column copy b (rows 7b..7b+12)
+      // as four independent 16-byte loads (a rolled per-row loop of dependent 4-byte loads
+      // cost ~4k cycles per pixel and warp)
 #pragma unroll 1
-      for (int tr = gr0; tr <= gr1 + KS - 1; ++tr) neq |= tile_at(T, tr, lane) != a0;
+      for (int b = 0; b < 3; ++b) {
+        float v[16];
+        load_col(T + copy_base(b) + lane * CS, v);
+#pragma unroll
+        for (int q = 0; q < SEGL + KS - 1; ++q) {
+          const int r = 7 * b + q;
+          neq |= r >= gr0 && r <= gr1 + KS - 1 && v[q] != a0;
+        }
+      }
     }
     const bool static_eq = !__any_sync(0xffffffffu, neq);
 
+#ifdef NLEM_LR_STAMPS
+    { const long long q_ = clock64(); st_p[0] += q_ - st_q; st_q = q_; }
+#endif
     // ---- distances ||a_k - a_self||^2 (patch.cpp:52-61), weights, lambdas; state init
     unsigned realmask = 0;  // bit s*7+i: grid point inside the clipped window (patch.cpp:72-76)
     float2 wgt[SEGL];  // (slot 0, slot 1) pairs
@@ -501,6 +519,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       }
       tm_st<16>(t_lam(), lm);
     }
+#ifdef NLEM_LR_STAMPS
+    { const long long q_ = clock64(); st_p[1] += q_ - st_q; st_q = q_; }
+#endif
 
     // ---- patch-sum pass (sum_k u_k a_k per coordinate) + transpose reduction to the owners.
     // Half A rows (jx - 0) * 7 + jy, half B rows (jx - 4) * 7 + jy, then 5 extra scalars.
@@ -546,6 +567,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       }
     };
 
+#ifdef NLEM_LR_STAMPS
+    { const long long q_ = clock64(); st_p[2] += q_ - st_q; st_q = q_; }
+#endif
     // ---- initial patch (nlem.cpp:13-18): weighted mean (ratio form) or the noisy patch.
     // Owner scalars in shared memory: rows 0 z_A, 1 z_B, 2 m_A, 3 m_B, 4.. c~ history ring
     // (slot (head - q) mod (R+1) holds c~_{t-q}), A then B.
@@ -577,6 +601,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       own[(4 + R + 1) * 32] = zB - mB;
       if (lane <= R) nrs[lane] = 0.0f;
     }
+#ifdef NLEM_LR_STAMPS
+    { const long long q_ = clock64(); st_p[3] += q_ - st_q; st_q = q_; }
+#endif
     int head = 0;
     // publish c~ (owners' ring head) and the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep
     auto publish = [&]() {
@@ -875,6 +902,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   if (blockIdx.x < 2 && lane == 0 && (warp == 0 || warp == 7) && st_n)
     printf("lr stamps blk %d warp %d: pixels %lld tile_wait %lld setup %lld sweeps %lld epilogue %lld (cycles/pixel)\n",
            blockIdx.x, warp, st_n, st_wait / st_n, st_setup / st_n, st_sw / st_n, st_epi / st_n);
+  if (blockIdx.x < 2 && lane == 0 && warp == 0 && st_n)
+    printf("lr setup: footprint %lld distances+weights+tmem %lld nlm-init(patch sum) %lld owners %lld\n",
+           st_p[0] / st_n, st_p[1] / st_n, st_p[2] / st_n, st_p[3] / st_n);
 #endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
