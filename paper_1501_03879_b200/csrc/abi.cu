@@ -412,7 +412,7 @@ nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t
   IrlsLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), x_init,
                cfg.epsilon, cfg.max_iter, cfg.tol, x_out, objective_out, iters_out,
                trace_objective, reinterpret_cast<FailureSlot*>(slot.ptr)};
-  e = launch_irls_generic(L, s);
+  e = irls_reg_supported(L) ? launch_irls_reg(L, s) : launch_irls_generic(L, s);
   if (e != cudaSuccess) return cuda_fail(failure, e);
   if (!failure) return NLEM_OK;
   unsigned long long v = ~0ull;

@@ -570,6 +570,237 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   cp_wait_all();
 }
 
+// ---------------------------------------------------------------------------------------
+// Batched IRLS (proj/include/nlem/irls.hpp:21-68), d = 49, 1 <= n <= 448: the same register
+// layout and consensus warp, direct differences (exact near coincident points, where epsilon
+// matters).  Pass p evaluates at x_p: per point D = ||x_p - a_k||^2 (FADD2 + FFMA2), root =
+// sqrt(D + eps), beta = w / root, the surrogate term w root (costs.hpp:24-33) and the cost term
+// w sqrt(D) (costs.hpp:13-20, the objective output at the final x); the point warps reduce
+// sum beta a, sum beta, the surrogate and the cost; the consensus warp applies the stop rule
+// (irls.hpp:58) and forms x_{p+1} = sum beta a / sum beta.  Failures are recorded as the
+// generic kernel does (iteration and kind of irls.hpp:39, :50, :52, :65-66).
+// ---------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(ALL, 1)
+irls_batched_reg(const float* __restrict__ points, const float* __restrict__ weights,
+                 int64_t batch, int n, const float* __restrict__ x_init, float eps, int T,
+                 float tol, float* x_out, float* obj_out, int* iters_out, float* tr_obj,
+                 FailureSlot* fail) {
+  extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
+  float* const red = smem + SM_RED;
+  float* const cb = smem + SM_CB;  // x of the coming pass
+  int* const ctl = reinterpret_cast<int*>(smem + SM_GR);
+  float* const scal = smem + SM_SCAL;
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int lane = tid & 31;
+  const int g = lane & (G - 1);
+  const int gid = warp * GPW + (lane >> 3);
+  const bool is_pts = warp < WARPS;
+  float* const myrow = red + (is_pts ? warp : 0) * RS;
+  auto point_of = [&](int q) { return 2 * ((q >> 1) * NG + gid) + (q & 1); };
+  const int k_me = point_of(g);
+  const bool real_me = is_pts && k_me < n;
+  const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
+  const int cj = 7 * cgrp + cidx;
+  const bool cv0 = cgrp < 7, cv1 = cgrp < 7 && (lane & 3) != 3;
+  const int nd = n * D;
+
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+
+  for (; b < batch; b += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();
+    const float* const st = stage + stage_shift(points + b * nd);
+    const float* const wv = wst + stage_shift(weights + b * n);
+    const bool greal = is_pts && g < 7;
+    float2 A[KP][J];
+    float2 wq[KP];
+#pragma unroll
+    for (int m = 0; m < KP; ++m) {
+      const int k0 = 2 * (m * NG + gid), k1 = k0 + 1;
+      const bool h0 = greal && k0 < n, h1 = greal && k1 < n;
+      wq[m] = make_float2(is_pts && k0 < n ? wv[k0] : 0.0f, is_pts && k1 < n ? wv[k1] : 0.0f);
+      const float* p0 = st + k0 * D + 7 * g;
+      const float* p1 = st + k1 * D + 7 * g;
+#pragma unroll
+      for (int i = 0; i < J; ++i) A[m][i] = make_float2(h0 ? p0[i] : 0.0f, h1 ? p1[i] : 0.0f);
+    }
+    const float w_me = real_me ? wv[k_me] : 0.0f;
+    __syncthreads();  // every thread is done with the stage
+    const int64_t bn = b + gridDim.x;
+    if (bn < batch) {
+      stage_copy(stage, points + bn * nd, nd);
+      stage_copy(wst, weights + bn * n, n);
+    }
+    cp_commit();
+
+    // ---- x_0: x_init, or the weighted mean points * (w / sum w) (irls.hpp:32, types.hpp:73)
+    if (x_init == nullptr) {
+      const float W = block_sum(w_me, scal, warp, lane);
+      const float rW = 1.0f / W;
+      float2 coef[KP];
+#pragma unroll
+      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x * rW, wq[m].y * rW);
+      float v[J];
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(coef[m], A[m][i], acc);
+        v[i] = acc.x + acc.y;
+      }
+      if (is_pts) fold_store(v, 0.0f, myrow, lane);
+      __syncthreads();
+    }
+    float x0 = 0.0f, x1 = 0.0f;  // consensus warp: x of the current pass at cj, cj + 1
+    if (warp == CW) {
+      if (x_init != nullptr) {
+        x0 = cv0 ? x_init[b * D + cj] : 0.0f;
+        x1 = cv1 ? x_init[b * D + cj + 1] : 0.0f;
+      } else {
+        const float2 s = rows_sum(red, lane);
+        x0 = cv0 ? s.x : 0.0f;
+        x1 = cv1 ? s.y : 0.0f;
+      }
+      reinterpret_cast<float2*>(cb)[lane] = make_float2(x0, x1);
+    }
+    __syncthreads();
+
+    float previous = 0.0f, obj = 0.0f;
+    int iters = T, fail_iter = -1, fail_kind = 0;
+    for (int p = 0;; ++p) {
+      if (is_pts) {
+        float xc[J];
+        load_coords(cb, g, xc);
+        float2 dq[KP];
+#pragma unroll
+        for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int i = 0; i < J; ++i) {
+#pragma unroll
+          for (int m = 0; m < KP; ++m) {
+            const float2 e = __fadd2_rn(f2(xc[i]), make_float2(-A[m][i].x, -A[m][i].y));
+            const float2 em = greal ? e : make_float2(0.0f, 0.0f);
+            dq[m] = __ffma2_rn(em, em, dq[m]);
+          }
+        }
+        const float d2 = group_rs8(dq, g);
+        const float root = sqrtf(d2 + eps);                       // irls.hpp:45-46
+        const float beta = real_me ? w_me / root : 0.0f;
+        const float sur = real_me ? w_me * root : 0.0f;           // costs.hpp:24-33
+        const float cost = real_me ? w_me * sqrtf(d2) : 0.0f;     // costs.hpp:13-20
+        float2 bq[KP];
+        group_ag8(beta, bq, lane);
+        float v[J];
+#pragma unroll
+        for (int i = 0; i < J; ++i) {
+          float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+          for (int m = 0; m < KP; ++m) acc = __ffma2_rn(bq[m], A[m][i], acc);
+          v[i] = acc.x + acc.y;
+        }
+        float hs;  // warp sums of (beta, surrogate, cost, 0) onto lanes r = lane & 3
+        {
+          const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
+          const float x0_ = (u2 ? cost : beta) + __shfl_xor_sync(0xffffffffu, u2 ? beta : cost, 2);
+          const float x1_ = (u2 ? 0.0f : sur) + __shfl_xor_sync(0xffffffffu, u2 ? sur : 0.0f, 2);
+          hs = (u1 ? x1_ : x0_) + __shfl_xor_sync(0xffffffffu, u1 ? x0_ : x1_, 1);
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+        }
+        fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
+      }
+      __syncthreads();
+      if (warp == CW) {
+        const float2 S = rows_sum(red, lane);
+        const float den = __shfl_sync(0xffffffffu, S.y, 3);
+        const float cur = __shfl_sync(0xffffffffu, S.y, 7);
+        const float cst = __shfl_sync(0xffffffffu, S.y, 11);
+        int c = 0;  // 0 continue, 1 done, 2 failed
+        bool next = false;
+        if (!isfinite(cur)) {  // irls.hpp:39 (x_0) / :52 (x_p)
+          fail_iter = p;
+          fail_kind = NLEM_FAIL_IRLS_OBJECTIVE;
+          c = 2;
+        } else if (p == 0) {
+          previous = cur;
+          next = true;
+        } else {
+          if (tr_obj != nullptr && lane == 0) tr_obj[b * T + p - 1] = cur;
+          if (previous - cur <= tol * fabsf(previous)) {  // irls.hpp:58
+            iters = p;
+            obj = cst;
+            c = 1;
+          } else if (p == T) {
+            obj = cst;
+            c = 1;
+          } else {
+            previous = cur;
+            next = true;
+          }
+        }
+        if (next) {  // x_{p+1} = sum beta a / sum beta (irls.hpp:48)
+          const float n0 = cv0 ? S.x / den : 0.0f, n1 = cv1 ? S.y / den : 0.0f;
+          if (__any_sync(0xffffffffu, !isfinite(n0) || !isfinite(n1))) {  // irls.hpp:50
+            fail_iter = p + 1;
+            fail_kind = NLEM_FAIL_IRLS_ITERATE;
+            c = 2;
+          } else {
+            x0 = n0;
+            x1 = n1;
+            reinterpret_cast<float2*>(cb)[lane] = make_float2(x0, x1);
+          }
+        }
+        if (lane == 0) *ctl = c;
+      }
+      __syncthreads();
+      if (*ctl != 0) break;
+    }
+    if (warp == CW) {
+      if (fail_iter >= 0) {
+        if (lane == 0) record_failure(fail, b, fail_iter, fail_kind);
+      } else {
+        if (cv0) x_out[b * D + cj] = x0;
+        if (cv1) x_out[b * D + cj + 1] = x1;
+        if (lane == 0) {
+          if (iters_out != nullptr) iters_out[b] = iters;
+          if (obj_out != nullptr) {
+            obj_out[b] = obj;
+            if (!isfinite(obj)) record_failure(fail, b, iters, NLEM_FAIL_IRLS_OBJECTIVE);
+          }
+        }
+      }
+    }
+  }
+  cp_wait_all();
+}
+
+bool irls_reg_supported(const IrlsLaunch& L) {
+  const char* force = std::getenv("NLEM_BATCHED");  // =fast: the generic IRLS kernel (A/B, tests)
+  if (force != nullptr && std::string(force) != "lr") return false;
+  return L.d == D && L.n >= 1 && L.n <= NCAP && L.batch < (int64_t(1) << 31) &&
+         static_cast<int64_t>(L.n) * D < (int64_t(1) << 31) / 4;
+}
+
+cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream) {
+  auto kfn = irls_batched_reg;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM_BYTES));
+  if (e != cudaSuccess) return e;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
+  kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
+      L.points, L.weights, L.batch, L.n, L.x_init, L.eps, L.max_iter, L.tol, L.x_out, L.obj_out,
+      L.iters_out, L.tr_obj, L.fail);
+  return cudaGetLastError();
+}
+
 bool admm_lr_supported(const AdmmLaunch& L) {
   const char* force = std::getenv("NLEM_BATCHED");  // =fast forces the p-form kernel (A/B, tests)
   if (force != nullptr && std::string(force) != "lr") return false;

@@ -94,6 +94,9 @@ cudaError_t launch_admm_fast_list(const AdmmLaunch& L, const int* list, const in
 // for launch_admm_fast_list.
 bool admm_lr_supported(const AdmmLaunch& L);
 cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cudaStream_t stream);
+// Register-resident batched IRLS for d = 49 (kernels_batched_lr.cu).
+bool irls_reg_supported(const IrlsLaunch& L);
+cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream);
 bool nlem_seg2_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_seg2(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);

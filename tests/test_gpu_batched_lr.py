@@ -160,3 +160,90 @@ def test_lr_numeric_failure_matches_pform(nb):
         msgs.append((str(e.value), e.value.iteration, e.value.index))
     assert msgs[0] == msgs[1]
     assert msgs[0][2] == 11
+
+
+# ------------------------------------------------------------------ batched IRLS (irls_batched_reg)
+def _irls(nb, pts, w, cfg, kernel):
+    import torch
+
+    old = dict(os.environ)
+    os.environ["NLEM_BATCHED"] = kernel
+    try:
+        r = nb.irls_euclidean_median(torch.from_numpy(np.ascontiguousarray(pts)).cuda()
+                                     if not hasattr(pts, "is_cuda") else pts,
+                                     torch.from_numpy(np.ascontiguousarray(w)).cuda()
+                                     if not hasattr(w, "is_cuda") else w, cfg)
+    finally:
+        os.environ.clear()
+        os.environ.update(old)
+    return r
+
+
+def test_irls_reg_config1_vs_oracle_and_generic(nb, oracle):
+    """irls.hpp:21-68 on config-1 problems at a fixed count (tol < 0): minimiser, objective and
+    the per-iteration surrogate trace vs the FP64 oracle; the generic kernel agrees."""
+    from paper_1501_03879_b200 import synth
+
+    pts, w = synth.point_sets(96)
+    cfg = nb.IrlsConfig(epsilon=1e-4, max_iter=30, tol=-1.0, record_trace=True)
+    r = _irls(nb, pts, w, cfg, "lr")
+    ref = oracle.irls_batched(pts.astype(np.float64), w.astype(np.float64), epsilon=1e-4,
+                              max_iter=30, tol=-1.0, trace=True)
+    z = r.minimizer.cpu().numpy()
+    assert np.abs(z - ref.minimizer).max() <= 1e-2
+    np.testing.assert_allclose(r.objective.cpu().numpy(), ref.objective, rtol=1e-5)
+    assert (r.iterations_run.cpu().numpy() == 30).all()
+    for b in range(0, 96, 7):
+        to = np.array([t.objective for t in r.trace[b]])
+        np.testing.assert_allclose(to, ref.trace_objective[b, :len(to)], rtol=1e-5)
+    g = _irls(nb, pts, w, cfg, "fast")
+    assert np.abs(z - g.minimizer.cpu().numpy()).max() <= 2e-3
+
+
+@pytest.mark.parametrize("n", [1, 2, 37, 448])
+def test_irls_reg_shapes_offsets_x_init_and_stop(nb, oracle, n):
+    """n = 1..448, every 4-byte offset of the device buffers mod 16, an explicit x_init, and the
+    stop rule (irls.hpp:58, tol = 0): the minimiser at the GPU's own stop iteration t equals the
+    oracle's x_t (a run of exactly t iterations)."""
+    import torch
+
+    rng = np.random.default_rng(7 + n)
+    B = 17
+    pts = rng.normal(128.0, 25.0, (B, n, 49)).astype(np.float32)
+    w = (1.0 - rng.random((B, n))).astype(np.float32)
+    cfg = nb.IrlsConfig(epsilon=1e-4, max_iter=20, tol=-1.0)
+    ref = oracle.irls_batched(pts.astype(np.float64), w.astype(np.float64), epsilon=1e-4,
+                              max_iter=20, tol=-1.0)
+    for off in range(4):
+        Pbig = torch.zeros(B * n * 49 + 4, device="cuda")
+        Pbig[off:off + B * n * 49] = torch.from_numpy(pts.reshape(-1)).cuda()
+        Wbig = torch.zeros(B * n + 4, device="cuda")
+        Wbig[3 - off:3 - off + B * n] = torch.from_numpy(w.reshape(-1)).cuda()
+        r = _irls(nb, Pbig[off:off + B * n * 49].view(B, n, 49), Wbig[3 - off:3 - off + B * n].view(B, n),
+                  cfg, "lr")
+        assert np.abs(r.minimizer.cpu().numpy() - ref.minimizer).max() <= 1e-2, off
+    xi = np.full(49, 60.0, np.float32)
+    r = _irls(nb, pts, w, nb.IrlsConfig(epsilon=1e-4, max_iter=6, tol=-1.0, x_init=xi), "lr")
+    ref = oracle.irls_batched(pts.astype(np.float64), w.astype(np.float64), epsilon=1e-4,
+                              max_iter=6, tol=-1.0, x_init=xi.astype(np.float64))
+    assert np.abs(r.minimizer.cpu().numpy() - ref.minimizer).max() <= 1e-2
+    r = _irls(nb, pts, w, nb.IrlsConfig(epsilon=1e-4, max_iter=40, tol=0.0), "lr")
+    its = r.iterations_run.cpu().numpy()
+    assert ((its >= 1) & (its <= 40)).all()
+    for b in range(B):
+        rb = oracle.irls_batched(pts[b:b + 1].astype(np.float64), w[b:b + 1].astype(np.float64),
+                                 epsilon=1e-4, max_iter=int(its[b]), tol=-1.0)
+        assert np.abs(r.minimizer.cpu().numpy()[b] - rb.minimizer[0]).max() <= 1e-2, b
+
+
+def test_irls_reg_numeric_failure_matches_generic(nb):
+    from paper_1501_03879_b200 import synth
+
+    pts, w = synth.point_sets(12)
+    w[5] = 3e38
+    msgs = []
+    for kernel in ("lr", "fast"):
+        with pytest.raises(nb.NumericFailure) as e:
+            _irls(nb, pts, w, nb.IrlsConfig(epsilon=1e-4, max_iter=5), kernel)
+        msgs.append((str(e.value), e.value.iteration, e.value.index))
+    assert msgs[0] == msgs[1] and msgs[0][2] == 5
