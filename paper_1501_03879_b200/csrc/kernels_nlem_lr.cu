@@ -672,10 +672,12 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         tm_ld16c_wait<2 * NF * SEGL>(tw, wl);
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
-          const float rx = sqrtf(d2[i].x + P.epsilon), ry = sqrtf(d2[i].y + P.epsilon);
-          beta[i] = make_float2(wl[2 * i] / rx, wl[2 * i + 1] / ry);  // irls.hpp:45-46
+          // one hardware reciprocal square root per point (rsqrt.approx, ~2 ulp)
+          const float sx = d2[i].x + P.epsilon, sy = d2[i].y + P.epsilon;
+          const float ix = rsq(sx), iy = rsq(sy);
+          beta[i] = make_float2(wl[2 * i] * ix, wl[2 * i + 1] * iy);  // irls.hpp:45-46
           bsum += beta[i].x + beta[i].y;
-          ssum += fmaf(wl[2 * i], rx, wl[2 * i + 1] * ry);  // costs.hpp:24-33
+          ssum += fmaf(wl[2 * i], sx * ix, wl[2 * i + 1] * (sy * iy));  // costs.hpp:24-33
         }
         float xA, xB, xs[5];
         {

@@ -72,6 +72,20 @@ def measure(problems=65536, reps=3):
         res[f"config1_{name}"] = {"problems_per_s": B / (ms / 1e3), "ms": ms,
                                   "tflops_algorithmic": flops / (ms / 1e3) / 1e12,
                                   "frac_fp32_peak": flops / (ms / 1e3) / 1e12 / PEAK}
+    # the IRLS surrogate solver (irls.hpp:21-68) on the same point sets: eps = 1e-4, T = 50
+    # sweeps at a fixed count (tol < 0); algorithmic work 5 d per point and sweep
+    icfg = L.IrlsConfigC()
+    icfg.epsilon, icfg.max_iter, icfg.tol = 1e-4, T, -1.0
+
+    def run_irls():
+        lib.nlem_irls_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d, None,
+                              icfg, C.c_void_p(z.data_ptr()), None, None, None, None,
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    ms = timed(run_irls, a.reps, flush)
+    flops = 5 * d * T * n * B
+    res["config1_irls"] = {"problems_per_s": B / (ms / 1e3), "ms": ms,
+                           "tflops_algorithmic": flops / (ms / 1e3) / 1e12,
+                           "frac_fp32_peak": flops / (ms / 1e3) / 1e12 / PEAK}
     res["config1_generation_s"] = gen_s
     del P, W
     # ---- config 2
