@@ -49,13 +49,21 @@ namespace lr {
 
 constexpr int KS = 7, SW = 21, HS = SW / 2;
 constexpr int TH = SW + KS - 1;  // 27
-// Tile layout: three column-major copies; copy b holds tile rows 7b .. 7b+12 (the rows the
-// segments of grid block b read), column x at CP_BASE[b] + x * CS, rows padded to 16 so a
-// segment's 13-value column is four 16-byte loads.  CS = 20 and the copy offsets put the 8 lanes
-// of each LDS.128 phase on distinct bank quads (252 wavefronts per sweep-column set vs 224 ideal).
-constexpr int CS = 20;
-constexpr int CP_B1 = 548, CP_B2 = 1096;
-constexpr int TILE = CP_B2 + TH * CS;  // 1636 floats
+// Tile layout: two PAIRED column-major copies.  A lane's two segments always read the same
+// relative (row, column) offsets, so their tile values are stored interleaved as (slot 0, slot 1)
+// float2 pairs and every correlation step is one FFMA2 on a pair:
+//  * copy A (lanes 0..20: segments (x, grid rows 0..6) and (x, rows 7..13)):
+//    A[x][r] = (T[r][x], T[r + 7][x]), r = 0..12, x = 0..26;
+//  * copy B (lanes 21..31: segments (x, rows 14..20) and (x + 11, rows 14..20), x = 0..10; lane
+//    31's second segment does not exist): B[x][r] = (T[14 + r][x], T[14 + r][x + 11]), x = 0..16.
+// A column is 14 pairs (pair 13 = 0 padding) = seven 16-byte loads; stride PCS = 28 floats (odd
+// number of 16-byte quads: 8 consecutive columns hit 8 distinct bank quads) and PB = PA + 12
+// mod 32 keeps the LDS.128 phase that straddles the two copies (lanes 16..23) conflict-free.
+constexpr int PCS = 28;
+constexpr int PA = 0, PB = 780;
+constexpr int BCOLS = 17;
+constexpr int TILE = PB + BCOLS * PCS;  // 1256 floats
+static_assert((PB - PA) % 32 == 12 && PB >= TH * PCS, "copy B placement");
 #ifndef NLEM_LR_WARPS
 #define NLEM_LR_WARPS 16
 #endif
@@ -214,16 +222,16 @@ __device__ __forceinline__ float box_clamp(float v, const nlem_box& box) {
   return (box.upper < y) ? box.upper : y;
 }
 
-// Segment geometry: vertical segment (grid column gx, grid rows 7b .. 7b+6).
+// Segment geometry: vertical segment (grid column gx, grid rows gy0 .. gy0+6) of a lane's slot.
 __device__ __forceinline__ void seg_of(int lane, int slot, int& gx, int& gy0, bool& valid) {
   valid = true;
-  if (slot == 0) {
-    if (lane < 21) { gx = lane; gy0 = 0; }
-    else { gx = lane - 21; gy0 = 7; }
+  if (lane < 21) {
+    gx = lane;
+    gy0 = slot ? 7 : 0;
   } else {
-    if (lane < 10) { gx = 11 + lane; gy0 = 7; }
-    else if (lane < 31) { gx = lane - 10; gy0 = 14; }
-    else { gx = 0; gy0 = 14; valid = false; }
+    gx = lane - 21 + (slot ? 11 : 0);
+    gy0 = 14;
+    valid = !(slot == 1 && lane == 31);
   }
 }
 
@@ -235,102 +243,45 @@ __device__ __forceinline__ float2 pin_pair(float2 v) {
   return make_float2(__uint_as_float(static_cast<unsigned>(b)), __uint_as_float(static_cast<unsigned>(b >> 32)));
 }
 
-__device__ __forceinline__ int copy_base(int b) { return b == 0 ? 0 : (b == 1 ? CP_B1 : CP_B2); }
-// tile element (row r, column x) in the copy that holds row r
+// tile element (row r, column x) in the paired copies
 __device__ __forceinline__ float tile_at(const float* T, int r, int x) {
-  const int b = r < 7 ? 0 : (r < 14 ? 1 : 2);
-  return T[copy_base(b) + x * CS + r - 7 * b];
+  if (r < 13) return T[PA + x * PCS + 2 * r];
+  if (r < 20) return T[PA + x * PCS + 2 * (r - 7) + 1];
+  return x < BCOLS ? T[PB + x * PCS + 2 * (r - 14)] : T[PB + (x - 11) * PCS + 2 * (r - 14) + 1];
 }
-// 16 values (13 used) of a segment column: four 16-byte loads.  The last quad is an opaque
-// ld.shared.v4 so the compiler does not shrink it to a 4-byte load of v[12] (a 4-byte load at
-// the 20-float column stride is a 4-way bank conflict; the 16-byte phases are conflict-free).
-__device__ __forceinline__ void load_col(const float* col, float (&v)[16]) {
+// the 14 pairs of a paired column: seven 16-byte loads
+__device__ __forceinline__ void load_pcol(const float* col, float2 (&v)[14]) {
 #pragma unroll
-  for (int q = 0; q < 3; ++q) {
+  for (int q = 0; q < 7; ++q) {
     const float4 t = reinterpret_cast<const float4*>(col)[q];
-    v[4 * q] = t.x;
-    v[4 * q + 1] = t.y;
-    v[4 * q + 2] = t.z;
-    v[4 * q + 3] = t.w;
+    v[2 * q] = make_float2(t.x, t.y);
+    v[2 * q + 1] = make_float2(t.z, t.w);
   }
-  asm("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-      : "=f"(v[12]), "=f"(v[13]), "=f"(v[14]), "=f"(v[15])
-      : "r"(su32(col + 12)));
 }
-// Even/odd accumulator pairs over the 7 points of a segment: a 7 x 7 correlation step
-// acc[i] += sum_jy f(v[i + jy], c[jy]) is issued as FFMA2 on aligned (v[2m], v[2m+1]) register
-// pairs: even jy updates points (0,1),(2,3),(4,5),(6); odd jy updates (1,2),(3,4),(5,6),(0).
-struct EO {
-  float2 e[3], o[3];
-  float e6, o0;
-  __device__ __forceinline__ void zero() {
+// acc[i] += v[i + jy] * c[jy]   (both slots of point i in one FFMA2)
+__device__ __forceinline__ void p_dot(float2 (&acc)[7], const float2 (&v)[14], const float (&c)[7]) {
 #pragma unroll
-    for (int m = 0; m < 3; ++m) e[m] = o[m] = make_float2(0.0f, 0.0f);
-    e6 = o0 = 0.0f;
-  }
-  __device__ __forceinline__ float get(int i) const {  // i compile-time after unrolling
-    const float ev = i == 6 ? e6 : (i & 1 ? e[i >> 1].y : e[i >> 1].x);
-    const float od = i == 0 ? o0 : (i & 1 ? o[i >> 1].x : o[(i - 1) >> 1].y);
-    return ev + od;
-  }
-};
-// acc[i] += v[i + jy] * c[jy]
-__device__ __forceinline__ void eo_dot(EO& a, const float (&v)[16], const float (&c)[KS]) {
+  for (int jy = 0; jy < 7; ++jy)
 #pragma unroll
-  for (int jy = 0; jy < KS; ++jy) {
-    const float2 cc = make_float2(c[jy], c[jy]);
-    if ((jy & 1) == 0) {
-#pragma unroll
-      for (int m = 0; m < 3; ++m) a.e[m] = __ffma2_rn(make_float2(v[2 * m + jy], v[2 * m + 1 + jy]), cc, a.e[m]);
-      a.e6 = fmaf(v[6 + jy], c[jy], a.e6);
-    } else {
-#pragma unroll
-      for (int m = 0; m < 3; ++m) a.o[m] = __ffma2_rn(make_float2(v[2 * m + 1 + jy], v[2 * m + 2 + jy]), cc, a.o[m]);
-      a.o0 = fmaf(v[jy], c[jy], a.o0);
-    }
-  }
+    for (int i = 0; i < 7; ++i) acc[i] = __ffma2_rn(v[i + jy], make_float2(c[jy], c[jy]), acc[i]);
 }
 // acc[i] += (v[i + jy] + nx[jy])^2   (nx = -x)
-__device__ __forceinline__ void eo_dist(EO& a, const float (&v)[16], const float (&nx)[KS]) {
+__device__ __forceinline__ void p_dist(float2 (&acc)[7], const float2 (&v)[14], const float (&nx)[7]) {
 #pragma unroll
-  for (int jy = 0; jy < KS; ++jy) {
-    const float2 cc = make_float2(nx[jy], nx[jy]);
-    if ((jy & 1) == 0) {
+  for (int jy = 0; jy < 7; ++jy)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const float2 d = __fadd2_rn(make_float2(v[2 * m + jy], v[2 * m + 1 + jy]), cc);
-        a.e[m] = __ffma2_rn(d, d, a.e[m]);
-      }
-      const float d6 = v[6 + jy] + nx[jy];
-      a.e6 = fmaf(d6, d6, a.e6);
-    } else {
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const float2 d = __fadd2_rn(make_float2(v[2 * m + 1 + jy], v[2 * m + 2 + jy]), cc);
-        a.o[m] = __ffma2_rn(d, d, a.o[m]);
-      }
-      const float d0 = v[jy] + nx[jy];
-      a.o0 = fmaf(d0, d0, a.o0);
+    for (int i = 0; i < 7; ++i) {
+      const float2 d = __fadd2_rn(v[i + jy], make_float2(nx[jy], nx[jy]));
+      acc[i] = __ffma2_rn(d, d, acc[i]);
     }
-  }
 }
-// g[jy] += u[i] * v[i + jy]: even i updates coordinates (0,1),(2,3),(4,5),(6); odd i (1,2),(3,4),(5,6),(0)
-__device__ __forceinline__ void eo_gsum(EO& g, const float (&v)[16], const float (&u)[SEGL]) {
+// g[jy] += u[i] * v[i + jy]   (slot 0 and slot 1 contributions in the two halves of g)
+__device__ __forceinline__ void p_gsum(float2 (&g)[7], const float2 (&v)[14], const float2 (&u)[7]) {
 #pragma unroll
-  for (int i = 0; i < SEGL; ++i) {
-    const float2 uu = make_float2(u[i], u[i]);
-    if ((i & 1) == 0) {
+  for (int i = 0; i < 7; ++i)
 #pragma unroll
-      for (int m = 0; m < 3; ++m) g.e[m] = __ffma2_rn(make_float2(v[i + 2 * m], v[i + 2 * m + 1]), uu, g.e[m]);
-      g.e6 = fmaf(v[i + 6], u[i], g.e6);
-    } else {
-#pragma unroll
-      for (int m = 0; m < 3; ++m) g.o[m] = __ffma2_rn(make_float2(v[i + 2 * m + 1], v[i + 2 * m + 2]), uu, g.o[m]);
-      g.o0 = fmaf(v[i], u[i], g.o0);
-    }
-  }
+    for (int jy = 0; jy < 7; ++jy) g[jy] = __ffma2_rn(u[i], v[i + jy], g[jy]);
 }
-
 // sum of red[row][0..31] (row stride RED_STR, 16-byte aligned) in a fixed tree order
 __device__ __forceinline__ float row_sum(const float* row) {
   float4 q[8];
@@ -388,7 +339,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   bool sval0, sval1;
   seg_of(lane, 0, sgx0, sgy00, sval0);
   seg_of(lane, 1, sgx1, sgy01, sval1);
-  const int soff0 = copy_base(sgy00 / 7) + sgx0 * CS, soff1 = copy_base(sgy01 / 7) + sgx1 * CS;
+  const int poff = lane < 21 ? PA + lane * PCS : PB + (lane - 21) * PCS;  // paired column base
   // coordinate owners: the reduction runs in two halves (patch columns 0-3 and 4-6); row
   // l of half A is coordinate (l % 7, l / 7), row l of half B is (l % 7, 4 + l / 7)
   const bool own0 = lane < 4 * KS, own1 = lane < 3 * KS;
@@ -404,22 +355,33 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     const int r = out_row0 + p / cols, c = p % cols;
     const float* src = pad + static_cast<int64_t>(r - out_row0) * pad_cols + c;
     (void)b;
-    if (lane < TH) {  // one tile column per lane, copy by copy (no hoisted per-element offsets)
-#pragma unroll
-      for (int cb_ = 0; cb_ < 3; ++cb_) {
-        float* dst = W + copy_base(cb_) + lane * CS;
-        const float* sp = src + static_cast<int64_t>(7 * cb_) * pad_cols + lane;
+    // 87 half-columns of 13 rows (A first / second halves of columns 0..26, B first halves of
+    // columns 0..16, B second halves of columns 0..15) in three uniform rounds over the lanes
+    // (a branch per copy would serialise the divergent paths)
+    auto half = [&](float* dst, const float* sp) {  // 13 rows of one tile column into pair slots
 #pragma unroll 1
-        for (int e = 0; e < SEGL + KS - 1; ++e, sp += pad_cols) cpa4(dst + e, sp);
-      }
+      for (int e = 0; e < SEGL + KS - 1; ++e, sp += pad_cols) cpa4(dst + 2 * e, sp);
+    };
+#pragma unroll 1
+    for (int rnd = 0; rnd < 3; ++rnd) {
+      const int j = rnd * 32 + lane;
+      int off, row0, col;
+      if (j < TH) { off = PA + j * PCS; row0 = 0; col = j; }
+      else if (j < 2 * TH) { off = PA + (j - TH) * PCS + 1; row0 = 7; col = j - TH; }
+      else if (j < 2 * TH + BCOLS) { off = PB + (j - 2 * TH) * PCS; row0 = 14; col = j - 2 * TH; }
+      else { off = PB + (j - 2 * TH - BCOLS) * PCS + 1; row0 = 14; col = j - 2 * TH - BCOLS + 11; }
+      if (j < 2 * TH + BCOLS + BCOLS - 1) half(W + off, src + static_cast<int64_t>(row0) * pad_cols + col);
     }
     cpa_commit();
   };
-  // the 3 padding rows of every column copy are read by the 16-byte column loads: keep them 0
-  for (int e = lane; e < 3 * TH * 3; e += 32) {
-    const int cp = e / (TH * 3), rem = e % (TH * 3);
-    W[copy_base(cp) + (rem / 3) * CS + 13 + rem % 3] = 0.0f;
+  // padding pair 13 of every paired column and the second half of B column 16 (tile column 27
+  // does not exist) are read by the 16-byte loads but never streamed in: keep them 0
+  for (int x = lane; x < TH + BCOLS; x += 32) {
+    float* col = W + (x < TH ? PA + x * PCS : PB + (x - TH) * PCS);
+    col[26] = 0.0f;
+    col[27] = 0.0f;
   }
+  if (lane < SEGL + KS - 1) W[PB + 16 * PCS + 2 * lane + 1] = 0.0f;
   if (pix < plane) issue_tile(pix, 0);
 
 #ifdef NLEM_LR_STAMPS
@@ -457,16 +419,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       // column `lane` of the footprint rows [gr0, gr1 + 6]: each column copy b (rows 7b..7b+12)
       // as four independent 16-byte loads (a rolled per-row loop of dependent 4-byte loads
       // cost ~4k cycles per pixel and warp)
-#pragma unroll 1
-      for (int b = 0; b < 3; ++b) {
-        float v[16];
-        load_col(T + copy_base(b) + lane * CS, v);
+      float2 v[14];
+      load_pcol(T + PA + lane * PCS, v);  // rows 0..12 (.x) and 7..19 (.y)
 #pragma unroll
-        for (int q = 0; q < SEGL + KS - 1; ++q) {
-          const int r = 7 * b + q;
-          neq |= r >= gr0 && r <= gr1 + KS - 1 && v[q] != a0;
-        }
+      for (int q = 0; q < SEGL + KS - 1; ++q) {
+        neq |= q >= gr0 && q <= gr1 + KS - 1 && v[q].x != a0;
+        neq |= q + 7 >= gr0 && q + 7 <= gr1 + KS - 1 && v[q].y != a0;
       }
+      const bool lo = lane < BCOLS;  // rows 14..26 of column `lane` in copy B
+      load_pcol(T + PB + (lo ? lane : lane - 11) * PCS, v);
+#pragma unroll
+      for (int q = 0; q < SEGL + KS - 1; ++q)
+        neq |= q + 14 >= gr0 && q + 14 <= gr1 + KS - 1 && (lo ? v[q].x : v[q].y) != a0;
     }
     const bool static_eq = !__any_sync(0xffffffffu, neq);
 
@@ -477,23 +441,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     unsigned realmask = 0;  // bit s*7+i: grid point inside the clipped window (patch.cpp:72-76)
     float2 wgt[SEGL];  // (slot 0, slot 1) pairs
     {
-      EO a0s, a1s;
-      a0s.zero();
-      a1s.zero();
+      float2 A2[SEGL];
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) A2[i] = make_float2(0.0f, 0.0f);
 #pragma unroll 1
       for (int jx = 0; jx < KS; ++jx) {
         float nac[KS];
 #pragma unroll
-        for (int jy = 0; jy < KS; ++jy) nac[jy] = -T[CP_B1 + (HS + jx) * CS + 3 + jy];  // a_self
-        float v[16];
-        load_col(T + soff0 + jx * CS, v);
-        eo_dist(a0s, v, nac);
-        load_col(T + soff1 + jx * CS, v);
-        eo_dist(a1s, v, nac);
+        for (int jy = 0; jy < KS; ++jy) nac[jy] = -tile_at(T, HS + jy, HS + jx);  // a_self
+        float2 v[14];
+        load_pcol(T + poff + jx * PCS, v);
+        p_dist(A2, v, nac);
       }
-      float2 A2[SEGL];
-#pragma unroll
-      for (int i = 0; i < SEGL; ++i) A2[i] = make_float2(a0s.get(i), a1s.get(i));
       float lm[16];
 #pragma unroll
       for (int s = 0; s < 2; ++s) {
@@ -530,24 +489,17 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int jxa = hf ? 4 : 0, jxb = hf ? KS : 4;
-        float u0[SEGL], u1[SEGL];
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) {
-          u0[i] = u2[i].x;
-          u1[i] = u2[i].y;
-        }
         LR_UNROLL(NLEM_LR_UG)
         for (int jx = jxa; jx < jxb; ++jx) {
-          EO g;
-          g.zero();
-          float v[16];
-          load_col(T + soff0 + jx * CS, v);
-          eo_gsum(g, v, u0);
-          load_col(T + soff1 + jx * CS, v);
-          eo_gsum(g, v, u1);
+          float2 g[KS];
+#pragma unroll
+          for (int jy = 0; jy < KS; ++jy) g[jy] = make_float2(0.0f, 0.0f);
+          float2 v[14];
+          load_pcol(T + poff + jx * PCS, v);
+          p_gsum(g, v, u2);
           float* rrow = red + (jx - jxa) * KS * RED_STR + lane;
 #pragma unroll
-          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = g.get(jy);
+          for (int jy = 0; jy < KS; ++jy) rrow[jy * RED_STR] = g[jy].x + g[jy].y;
         }
         if (hf) {
 #pragma unroll
@@ -574,8 +526,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // Owner scalars in shared memory: rows 0 z_A, 1 z_B, 2 m_A, 3 m_B, 4.. c~ history ring
     // (slot (head - q) mod (R+1) holds c~_{t-q}), A then B.
     {
-      const float mA = own0 ? T[CP_B1 + (HS + jx0) * CS + 3 + jy0] : 0.0f;
-      const float mB = own1 ? T[CP_B1 + (HS + jx1) * CS + 3 + jy0] : 0.0f;
+      const float mA = own0 ? tile_at(T, HS + jy0, HS + jx0) : 0.0f;
+      const float mB = own1 ? tile_at(T, HS + jy0, HS + jx1) : 0.0f;
       float zA = mA, zB = mB;
       if (nlm_init) {
         float ex[5] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
@@ -649,23 +601,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         if (own0) cb[jx0 * CB_STR + jy0] = own[0];
         if (own1) cb[jx1 * CB_STR + jy0] = own[32];
         __syncwarp();
-        EO e0, e1;
-        e0.zero();
-        e1.zero();
+        float2 d2[SEGL];
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) d2[i] = make_float2(0.0f, 0.0f);
 #pragma unroll 1
         for (int jx = 0; jx < KS; ++jx) {
           float nx[KS];
 #pragma unroll
           for (int jy = 0; jy < KS; ++jy) nx[jy] = -cb[jx * CB_STR + jy];
-          float v[16];
-          load_col(T + soff0 + jx * CS, v);
-          eo_dist(e0, v, nx);
-          load_col(T + soff1 + jx * CS, v);
-          eo_dist(e1, v, nx);
+          float2 v[14];
+          load_pcol(T + poff + jx * PCS, v);
+          p_dist(d2, v, nx);
         }
-        float2 d2[SEGL];
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) d2[i] = make_float2(e0.get(i), e1.get(i));
         float2 beta[SEGL];
         float bsum = 0.0f, ssum = 0.0f;
         float wl[16];
@@ -727,9 +674,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       bool fnorm = false, sne1 = false;
       float2 Dk2[SEGL];
       {
-        EO d0, d1;
-        d0.zero();
-        d1.zero();
+#pragma unroll
+        for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(0.0f, 0.0f);
         LR_UNROLL(NLEM_LR_UD)
         for (int jx = 0; jx < KS; ++jx) {
           float cvx[KS];  // column jx of c~ (two broadcast 16-byte loads)
@@ -739,14 +685,10 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
             cvx[0] = ca.x; cvx[1] = ca.y; cvx[2] = ca.z; cvx[3] = ca.w;
             cvx[4] = cc.x; cvx[5] = cc.y; cvx[6] = cc.z;
           }
-          float v[16];
-          load_col(T + soff0 + jx * CS, v);
-          eo_dot(d0, v, cvx);
-          load_col(T + soff1 + jx * CS, v);
-          eo_dot(d1, v, cvx);
+          float2 v[14];
+          load_pcol(T + poff + jx * PCS, v);
+          p_dot(Dk2, v, cvx);
         }
-#pragma unroll
-        for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(d0.get(i), d1.get(i));
       }
       {
         float lm[16];
