@@ -58,7 +58,7 @@ _VARIANT_TOKENS = {
     "xw4": "-DNLEM_TILE_XW=4",       # warp pre-reduction + CPT consensus, split p-form
     "lrw12": "-DNLEM_LR_WARPS=12",   # low-rank kernel with 12 pixel-warps per SM (168 registers)
     "lrw14": "-DNLEM_LR_WARPS=14",
-    "ud7": "-DNLEM_LR_UD=7",         # low-rank kernel: unrolled dot-product column loop
+    "ud1": "-DNLEM_LR_UD=1",         # low-rank kernel: rolled dot-product column loop (default 7)
     "ug4": "-DNLEM_LR_UG=4",         # low-rank kernel: unrolled patch-sum column loop
     "st1": "-DNLEM_LR_ST=1",         # low-rank kernel: columns per TMEM store in the sweep
     "st4": "-DNLEM_LR_ST=4",

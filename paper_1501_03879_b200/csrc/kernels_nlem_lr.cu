@@ -73,7 +73,7 @@ constexpr int R = 4;     // history ring
 constexpr int NF = 8;    // state fields per point in TMEM
 // unroll factors of the correlation loops over patch columns (A/B build variants)
 #ifndef NLEM_LR_UD
-#define NLEM_LR_UD 1
+#define NLEM_LR_UD 7  // A/B on the paired layout: 7 (unrolled) 32.23 vs 1 (rolled) 32.00 Mpix/s
 #endif
 #ifndef NLEM_LR_UG
 #define NLEM_LR_UG 1
