@@ -134,6 +134,23 @@ def load_profile_traffic():
         return None
 
 
+def load_profile_pipes():
+    """Executed-work utilisation of the dominant kernel (committed ncu summary): explains a
+    roofline fraction above 1 (the algorithmic count exceeds the low-rank form's executed work)."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"fma_pipe_active_pct": d.get("fma_pipe_active_pct"),
+                "issue_active_pct": d.get("issue_active_pct"), "source": d.get("pipe_source"),
+                "note": "frac is algorithmic: 12 flops per (pixel, neighbour, coordinate, sweep) "
+                        "as SURVEY.md 8(d) counts Algorithm 1; the low-rank (Gram-form) kernel "
+                        "executes about a third of them, so frac can exceed 1 while the FP32 pipe "
+                        "is busy fma_pipe_active_pct of the time"}
+    except Exception:
+        return None
+
+
 def cpu_reference(noisy, params_kw, sample_rows, threads):
     """Time the FP64 oracle (restated reference) on a row sample; returns (Mpix/s, seconds)."""
     from oracle import oracle as O
@@ -360,6 +377,7 @@ def main():
         "roofline": {"bound": "fp32", "achieved": float(achieved_t.item()), "peak": peak,
                      "unit": "TFLOP/s", "frac": float(achieved_t.item()) / peak,
                      "traffic": load_profile_traffic(),
+                     "executed": load_profile_pipes(),
                      "peak_source": "derived 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (no FP32 "
                                     "figure in MEASURED_PEAKS.json)",
                      "kernel": "nlem pixel kernel (+pad), per-step CUDA events",

@@ -8,7 +8,7 @@ python tools/ncu_lines.py gpurun_out/prof_lr_full.ncu-rep 40 > profiles/${tag}_l
 python tools/dev/ncu_brief.py gpurun_out/prof_lr_full.ncu-rep > profiles/${tag}_lr_brief.txt
 python tools/dev/ncu_ops.py gpurun_out/prof_lr_full.ncu-rep > profiles/${tag}_lr_opcodes.txt 2>/dev/null || true
 python tools/dev/ncu_stall_ops.py gpurun_out/prof_lr_full.ncu-rep > profiles/${tag}_lr_stalls.txt
-python - <<'PY'
+TAG=$tag python - <<'PY'
 import csv, collections, json
 rows = list(csv.reader(open('gpurun_out/launches.csv')))
 hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
@@ -34,6 +34,13 @@ m = {}
 for r in rows[hi + 1:]:
     d = dict(zip(h, r)); m[d['Metric Name']] = float(d['Metric Value'].replace(',', ''))
 rec = json.load(open('profiles/ncu_summary.json'))
+import glob, os, sys
+tag = os.environ.get("TAG")
+v = json.load(open(f'profiles/{tag}_lr_ncu.json'))[0] if tag else {}
+if v:
+    rec.update({"fma_pipe_active_pct": v["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"],
+                "issue_active_pct": v["smsp__issue_active.avg.pct_of_peak_sustained_active"],
+                "pipe_source": f"profiles/{tag}_lr_ncu.json (ncu --set full, one 131k-pixel launch of nlem_pixels_lr)"})
 rec.update({"dram_bytes_read": m['dram__bytes_read.sum'], "dram_bytes_write": m['dram__bytes_write.sum'],
             "dram_bytes_per_launch": m['dram__bytes_read.sum'] + m['dram__bytes_write.sum'],
             "gpu_time_ns_under_ncu": m['gpu__time_duration.sum']})
