@@ -12,22 +12,26 @@
 //     z_t = P_C(z_{t-1} - g/n),  g = sum_r (sum_k al'_r) c~_{t-r} - sum_k ga'_k a~_k,
 //     c~_{t+1} = 2 z_t - z_{t-1} - m.
 // A problem whose history ring would drop a term above FP32 rounding of p (2^-22 ||p||), whose
-// points are all equal (the exact-stop case of admm.hpp:77, tested structurally by the p-form
-// kernel), or that produces a non-finite value is handed, through a device-side list, to the
-// exact p-form kernel (admm_batched_fast), which then owns its outputs and failure record.
+// ||p||^2 expansion cancels (N < 2^-8 (H + ||c~||^2)), whose points are all equal (the
+// exact-stop case of admm.hpp:77, tested structurally by the p-form kernel), or that produces a
+// non-finite value is handed, through a device-side list, to the exact p-form kernel
+// (admm_batched_fast), which then owns its outputs and failure record.
 //
-// Mapping (B200): one problem per CTA of 14 warps, 1 CTA per SM.
+// Mapping (B200): one problem per CTA of 14 point warps + 1 consensus warp, 1 CTA per SM.
 //  * the centred points live in REGISTERS (the p-form kernel kept them in shared memory and
-//    re-read them every sweep): groups of 8 lanes own 8 points, each lane 7 coordinates
-//    (j = 8 i + g, d padded to 56) as float2 point pairs, so both passes are FFMA2;
+//    re-read them every sweep): groups of 8 lanes own 8 points, each lane 7 contiguous
+//    coordinates (j = 7 g + i, d padded to 56) as float2 point pairs, so both passes are FFMA2;
 //  * lane g of a group owns the scalar state of point slot g: reduce-scatter of the 8 dot
 //    products in the group, scalar update, all-gather of ga';
-//  * one CTA barrier per sweep: per-warp column partials (double-buffered rows), then EVERY
-//    warp redundantly finishes the consensus for all coordinates (lane l: j = l, l + 32) in the
-//    same fixed order, so all warps hold bitwise identical z, c~ and Gram rows without a second
-//    barrier;
+//  * each point warp folds its 4 groups and writes one 64-column partial row (coordinates at
+//    columns 8 g + i, history sums sum_k al'_r in columns 8 r + 7); after the CTA barrier the
+//    consensus warp sums the 14 rows in a fixed tree, forms z_t and c~_{t+1}, publishes c~
+//    (named barrier 1) and then the Gram row (named barrier 2), so the point warps' dot products
+//    overlap the Gram reduction; ptxas moves arithmetic across bar.sync, so the order is pinned
+//    with a shared-memory store before each wait and a reload after the arrive;
 //  * the next problem's points and weights stream into a shared-memory staging buffer with
 //    16-byte cp.async during the current problem's sweeps.
+// The batched IRLS kernel (irls_batched_reg, below) reuses the layout and the consensus warp.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
