@@ -24,18 +24,19 @@
 //
 // Mapping (B200): ONE PIXEL PER WARP, 16 independent pixel-warps per SM - no CTA barrier on
 // the sweep path, so one warp's reduction latency is hidden by the other fifteen's FMAs.
-//  * the pixel's 27 x 27 image tile sits in shared memory (row stride 35: the 32 lanes' column
-//    segments start on 32 distinct banks), double-buffered: the next pixel's tile streams in
-//    with cp.async during the current pixel's sweeps;
-//  * lane l owns two vertical segments of 7 grid points (63 segments = 441 points); a column
-//    of 13 tile values serves 49 FMAs of the dot products (and of the patch sums);
+//  * lane l owns two vertical segments of 7 grid points (63 segments = 441 points) that read
+//    the same relative tile offsets, so the pixel's 27 x 27 tile sits in shared memory as two
+//    PAIRED column-major copies ((slot 0, slot 1) float2 per tile row, see the layout below):
+//    a paired column (seven 16-byte loads) serves 49 FFMA2 of the dot products, the distances
+//    and the patch sums.  The tile streams in with 4-byte cp.async at the end of the previous
+//    pixel (its latency is not exposed: other warps compute);
 //  * the per-point state (8 x 32-bit) lives in TENSOR MEMORY: 14 points x 8 columns + 14
 //    lambdas per lane = 128 columns per warp, 16 warps = all 512 columns x 128 lanes of the SM,
-//    moved with tcgen05.ld/st 32x32b.x8 - registers stay free for the FMA working set;
+//    moved with tcgen05.ld x16 / st x2 - registers stay free for the FMA working set;
 //  * the 54 per-lane partials (49 coordinates, sum ga, 4 history sums) are reduced with a
 //    shared-memory transpose (fixed tree: bitwise deterministic), the 49 consensus coordinates
-//    are finished by their owner lanes, which keep z, m and the c~ history in registers; the
-//    Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce.
+//    are finished by their owner lanes, which keep z, m and the c~ history in shared memory;
+//    the Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
