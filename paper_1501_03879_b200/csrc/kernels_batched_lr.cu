@@ -191,17 +191,40 @@ __device__ __forceinline__ void load_coords(const float* row, int g, float (&c)[
   c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
   c[4] = b.x; c[5] = b.y; c[6] = b.z;
 }
-// Block sum of one value per thread (fixed order).  Contains two barriers.
-__device__ __forceinline__ float block_sum(float v, float* scal, int warp, int lane) {
+// Block sum of one value per thread (fixed order), valid in thread 0 only.  One barrier: the
+// next write of `scal` happens after the next problem's top-of-loop barrier.
+__device__ __forceinline__ float block_sum0(float v, float* scal, int warp, int lane) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if (lane == 0) scal[warp] = v;
   __syncthreads();
   float t = 0.0f;
+  if (threadIdx.x == 0)
 #pragma unroll
-  for (int w = 0; w < NW; ++w) t += scal[w];
-  __syncthreads();
+    for (int w = 0; w < NW; ++w) t += scal[w];
   return t;
+}
+
+// Weighted-mean numerator and denominator in one row pass (admm.hpp:40 / irls.hpp:32 with
+// types.hpp:71-74): the point warps write sum_k w_k a_k per coordinate and the weight sum (column
+// 7) into their partial rows; one barrier; the consensus warp divides (sum w a) / (sum w).
+__device__ __forceinline__ void weighted_sum_rows(const float2 (&A)[KP][J], const float2 (&wq)[KP],
+                                                  float* myrow, bool is_pts, int lane) {
+  float v[J];
+#pragma unroll
+  for (int i = 0; i < J; ++i) {
+    float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+    for (int m = 0; m < KP; ++m) acc = __ffma2_rn(wq[m], A[m][i], acc);
+    v[i] = acc.x + acc.y;
+  }
+  float ws = 0.0f;  // weights of this lane's group (same in its 8 lanes), then of the warp
+#pragma unroll
+  for (int m = 0; m < KP; ++m) ws += wq[m].x + wq[m].y;
+  ws += __shfl_xor_sync(0xffffffffu, ws, 8);
+  ws += __shfl_xor_sync(0xffffffffu, ws, 16);
+  if (is_pts) fold_store(v, lane == 0 ? ws : 0.0f, myrow, lane);
+  __syncthreads();
 }
 
 }  // namespace blr
@@ -306,31 +329,16 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #endif
     // ---- z_0 = m: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
     float m0 = 0.0f, m1 = 0.0f;  // consensus warp: m at coordinates cj, cj + 1
-    if (z_init == nullptr) {
-      const float W = block_sum(w_me, scal, warp, lane);
-      float2 coef[KP];
-      const float rW = 1.0f / W;
-#pragma unroll
-      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x * rW, wq[m].y * rW);
-      float v[J];
-#pragma unroll
-      for (int i = 0; i < J; ++i) {
-        float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(coef[m], A[m][i], acc);
-        v[i] = acc.x + acc.y;
-      }
-      if (is_pts) fold_store(v, 0.0f, myrow, lane);
-      __syncthreads();
-    }
+    if (z_init == nullptr) weighted_sum_rows(A, wq, myrow, is_pts, lane);
     if (warp == CW) {
       if (z_init != nullptr) {
         m0 = cv0 ? z_init[b * D + cj] : 0.0f;
         m1 = cv1 ? z_init[b * D + cj + 1] : 0.0f;
       } else {
         const float2 s = rows_sum(red, lane);
-        m0 = cv0 ? s.x : 0.0f;
-        m1 = cv1 ? s.y : 0.0f;
+        const float W = __shfl_sync(0xffffffffu, s.y, 3);  // sum of the weights (column 7)
+        m0 = cv0 ? s.x / W : 0.0f;
+        m1 = cv1 ? s.y / W : 0.0f;
       }
       reinterpret_cast<float2*>(mb)[lane] = make_float2(m0, m1);
       reinterpret_cast<float2*>(cb)[lane] = make_float2(0.0f, 0.0f);  // c~_1 = z_0 - m = 0
@@ -555,7 +563,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         }
       }
       const float dist2 = group_rs8(dq, g);
-      const float obj = block_sum(real_me ? w_me * sqrtf(dist2) : 0.0f, scal, warp, lane);
+      const float obj = block_sum0(real_me ? w_me * sqrtf(dist2) : 0.0f, scal, warp, lane);
       if (tid == 0) {
         obj_out[b] = obj;
         if (!isfinite(obj)) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
@@ -595,7 +603,6 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   float* const red = smem + SM_RED;
   float* const cb = smem + SM_CB;  // x of the coming pass
   int* const ctl = reinterpret_cast<int*>(smem + SM_GR);
-  float* const scal = smem + SM_SCAL;
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int lane = tid & 31;
@@ -646,23 +653,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
     cp_commit();
 
     // ---- x_0: x_init, or the weighted mean points * (w / sum w) (irls.hpp:32, types.hpp:73)
-    if (x_init == nullptr) {
-      const float W = block_sum(w_me, scal, warp, lane);
-      const float rW = 1.0f / W;
-      float2 coef[KP];
-#pragma unroll
-      for (int m = 0; m < KP; ++m) coef[m] = make_float2(wq[m].x * rW, wq[m].y * rW);
-      float v[J];
-#pragma unroll
-      for (int i = 0; i < J; ++i) {
-        float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(coef[m], A[m][i], acc);
-        v[i] = acc.x + acc.y;
-      }
-      if (is_pts) fold_store(v, 0.0f, myrow, lane);
-      __syncthreads();
-    }
+    if (x_init == nullptr) weighted_sum_rows(A, wq, myrow, is_pts, lane);
     float x0 = 0.0f, x1 = 0.0f;  // consensus warp: x of the current pass at cj, cj + 1
     if (warp == CW) {
       if (x_init != nullptr) {
@@ -670,8 +661,9 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
         x1 = cv1 ? x_init[b * D + cj + 1] : 0.0f;
       } else {
         const float2 s = rows_sum(red, lane);
-        x0 = cv0 ? s.x : 0.0f;
-        x1 = cv1 ? s.y : 0.0f;
+        const float W = __shfl_sync(0xffffffffu, s.y, 3);  // sum of the weights (column 7)
+        x0 = cv0 ? s.x / W : 0.0f;
+        x1 = cv1 ? s.y / W : 0.0f;
       }
       reinterpret_cast<float2*>(cb)[lane] = make_float2(x0, x1);
     }
