@@ -247,3 +247,31 @@ def test_irls_reg_numeric_failure_matches_generic(nb):
             _irls(nb, pts, w, nb.IrlsConfig(epsilon=1e-4, max_iter=5), kernel)
         msgs.append((str(e.value), e.value.iteration, e.value.index))
     assert msgs[0] == msgs[1] and msgs[0][2] == 5
+
+
+def test_batched_kernels_bitwise_deterministic_and_order_independent(nb):
+    """Race check without a sanitizer: every problem's result is bitwise independent of the run,
+    of its position in the batch (another CTA, another prefetch/staging shift) and of the batch
+    size, for the batched ADMM and IRLS kernels (fixed reduction trees, no float atomics)."""
+    import torch
+    from paper_1501_03879_b200 import synth
+
+    pts, w = synth.point_sets(300)
+    perm = np.random.default_rng(5).permutation(300)
+    box = nb.BoxConstraint.interval(0.0, 255.0)
+    cfg = nb.AdmmConfig(mu=1.0, max_iter=20)
+    icfg = nb.IrlsConfig(epsilon=1e-4, max_iter=15, tol=-1.0)
+    outs = []
+    for kernel_cfg, fn in ((cfg, lambda P, W, c: nb.admm_euclidean_median(P, W, box, c)),
+                           (icfg, lambda P, W, c: nb.irls_euclidean_median(P, W, c))):
+        P, W = torch.from_numpy(pts).cuda(), torch.from_numpy(w).cuda()
+        a = fn(P, W, kernel_cfg)
+        b = fn(P, W, kernel_cfg)
+        za, zb = a.minimizer.cpu().numpy(), b.minimizer.cpu().numpy()
+        assert np.array_equal(za, zb)
+        assert np.array_equal(a.objective.cpu().numpy(), b.objective.cpu().numpy())
+        c = fn(P[perm].contiguous(), W[perm].contiguous(), kernel_cfg)
+        assert np.array_equal(c.minimizer.cpu().numpy(), za[perm])
+        d = fn(P[137:].contiguous(), W[137:].contiguous(), kernel_cfg)  # other staging shifts
+        assert np.array_equal(d.minimizer.cpu().numpy(), za[137:])
+        outs.append(za)
