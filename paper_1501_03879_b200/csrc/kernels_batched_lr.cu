@@ -682,9 +682,10 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
         for (int i = 0; i < J; ++i) {
 #pragma unroll
           for (int m = 0; m < KP; ++m) {
+            // no mask for the padding coordinates of lanes g = 7: their points are 0 and x's
+            // padding columns are written as exact zeros (cv0 / cv1), so e = 0 there
             const float2 e = __fadd2_rn(f2(xc[i]), make_float2(-A[m][i].x, -A[m][i].y));
-            const float2 em = greal ? e : make_float2(0.0f, 0.0f);
-            dq[m] = __ffma2_rn(em, em, dq[m]);
+            dq[m] = __ffma2_rn(e, e, dq[m]);
           }
         }
         const float d2 = group_rs8(dq, g);

@@ -1,5 +1,5 @@
 """Small fixed workload for ncu captures: one NLEM launch on a row band of the config-3
-image (same kernel, same per-pixel work as the bench), or a config-1 batch."""
+image (same kernel, same per-pixel work as the bench), or a config-1 batch (ADMM or IRLS)."""
 import argparse
 import math
 import os
@@ -13,7 +13,7 @@ import paper_1501_03879_b200 as nb
 from paper_1501_03879_b200 import synth
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--what", default="nlem", choices=["nlem", "admm"])
+ap.add_argument("--what", default="nlem", choices=["nlem", "admm", "irls"])
 ap.add_argument("--rows", type=int, default=32)
 ap.add_argument("--problems", type=int, default=2048)
 ap.add_argument("--reps", type=int, default=2)
@@ -30,6 +30,9 @@ else:
     pts, w = synth.point_sets(a.problems)
     P, W = torch.from_numpy(pts).cuda(), torch.from_numpy(w).cuda()
     for _ in range(a.reps):
-        r = nb.admm_euclidean_median(P, W, nb.BoxConstraint.interval(0, 255), nb.AdmmConfig(mu=1.0, max_iter=50))
+        if a.what == "admm":
+            r = nb.admm_euclidean_median(P, W, nb.BoxConstraint.interval(0, 255), nb.AdmmConfig(mu=1.0, max_iter=50))
+        else:  # the batched IRLS comparator at config-1 shapes, fixed count (tol < 0)
+            r = nb.irls_euclidean_median(P, W, nb.IrlsConfig(epsilon=1e-4, max_iter=50, tol=-1.0))
 torch.cuda.synchronize()
 print("done")
