@@ -62,15 +62,20 @@ constexpr float kCancel = 1.0f / 256.0f;           // N below 2^-8 (H + ||c~||^2
 constexpr int SM_STAGE = 0;                      // raw points of the next problem (+4 shift)
 constexpr int SM_WST = SM_STAGE + NCAP * D + 4;  // raw weights of the next problem (+4 shift)
 constexpr int SM_RED = SM_WST + NCAP + 4;        // [WARPS][RS] per-warp partial rows
-constexpr int SM_CB = SM_RED + WARPS * RS;       // [RS] c~ of the coming sweep
-constexpr int SM_MB = SM_CB + RS;                // [RS] m (centring), then z~ for the cost
-constexpr int SM_GR = SM_MB + RS;                // [8] Gram row: G_0..G_3, ||c~||^2, ||c~_{t-4}||^2
+// Published rows (c~ / x, m) are read by every point lane as two 16-byte loads at column 8 g:
+// columns 32..63 sit 4 floats further on (RSK = RS + 4), so lanes g and g + 4 hit distinct banks
+// (one wavefront per load instead of two; these loads follow the row barrier on every warp).
+constexpr int RSK = RS + 4;
+constexpr int SM_CB = SM_RED + WARPS * RS;       // [RSK] c~ of the coming sweep (skewed)
+constexpr int SM_MB = SM_CB + RSK;               // [RSK] m (centring), then z~ for the cost (skewed)
+constexpr int SM_GR = SM_MB + RSK;               // [8] Gram row: G_0..G_3, ||c~||^2, ||c~_{t-4}||^2
 constexpr int SM_SCAL = SM_GR + 8;               // [32] block-sum scratch
 constexpr int SM_PIN = SM_SCAL + 32;             // [ALL] barrier-ordering scratch
 constexpr int SM_TOTAL = SM_PIN + ALL;
 constexpr size_t SMEM_BYTES = size_t(SM_TOTAL) * sizeof(float);
 static_assert(NCAP >= 441, "config-1 capacity");
-static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_GR % 4 == 0, "alignment");
+static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_MB % 4 == 0 &&
+              SM_GR % 4 == 0, "alignment");
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -184,10 +189,18 @@ __device__ __forceinline__ float2 rows_sum(const float* red, int lane) {
     for (int w = 0; w + span < WARPS; w += 2 * span) r[w] = __fadd2_rn(r[w], r[w + span]);
   return r[0];
 }
+// columns 2 l, 2 l + 1 of a published row: the consensus lane l's pair.  SKEW (ADMM): columns
+// 32..63 4 floats on; the IRLS kernel measured 1.5 % slower with the skew and keeps the plain row.
+template <bool SKEW = true>
+__device__ __forceinline__ float2* pub_pair(float* row, int lane) {
+  return reinterpret_cast<float2*>(row + 2 * lane + (SKEW ? ((lane >> 4) << 2) : 0));
+}
 // the 7 coordinates (8 columns) of lane g of a group from a published row
+template <bool SKEW = true>
 __device__ __forceinline__ void load_coords(const float* row, int g, float (&c)[J]) {
-  const float4 a = reinterpret_cast<const float4*>(row + 8 * g)[0];
-  const float4 b = reinterpret_cast<const float4*>(row + 8 * g)[1];
+  const float* const base = row + 8 * g + (SKEW ? ((g >> 2) << 2) : 0);
+  const float4 a = reinterpret_cast<const float4*>(base)[0];
+  const float4 b = reinterpret_cast<const float4*>(base)[1];
   c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w;
   c[4] = b.x; c[5] = b.y; c[6] = b.z;
 }
@@ -340,8 +353,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         m0 = cv0 ? s.x / W : 0.0f;
         m1 = cv1 ? s.y / W : 0.0f;
       }
-      reinterpret_cast<float2*>(mb)[lane] = make_float2(m0, m1);
-      reinterpret_cast<float2*>(cb)[lane] = make_float2(0.0f, 0.0f);  // c~_1 = z_0 - m = 0
+      *pub_pair(mb, lane) = make_float2(m0, m1);
+      *pub_pair(cb, lane) = make_float2(0.0f, 0.0f);  // c~_1 = z_0 - m = 0
       if (lane < 8) gr[lane] = 0.0f;
     }
     __syncthreads();
@@ -486,10 +499,10 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         const float c1 = cv1 ? (2.0f * zn1 - z1) - m1 : 0.0f;
         z0 = zn0;
         z1 = zn1;
-        reinterpret_cast<float2*>(cb)[lane] = make_float2(c0, c1);
+        *pub_pair(cb, lane) = make_float2(c0, c1);
         __syncwarp();
         if (t < T) bar_arrive(BAR_C);
-        const float2 cg = reinterpret_cast<const float2*>(cb)[lane];  // Gram after the arrive
+        const float2 cg = *pub_pair(cb, lane);  // Gram after the arrive
         const float c0g = cg.x, c1g = cg.y;
         float part[R + 1];
 #pragma unroll
@@ -545,7 +558,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     if (iters_out != nullptr && tid == 0) iters_out[b] = T;
     if (obj_out != nullptr) {
       // em_cost(z) = sum_k w_k ||z - a_k|| (costs.hpp:13-20), z - a = (z - m) - a~
-      if (warp == CW) reinterpret_cast<float2*>(mb)[lane] = make_float2(z0 - m0, z1 - m1);
+      if (warp == CW) *pub_pair(mb, lane) = make_float2(z0 - m0, z1 - m1);
       __syncthreads();
       float zc[J];
       load_coords(mb, g, zc);
@@ -665,7 +678,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
         x0 = cv0 ? s.x / W : 0.0f;
         x1 = cv1 ? s.y / W : 0.0f;
       }
-      reinterpret_cast<float2*>(cb)[lane] = make_float2(x0, x1);
+      *pub_pair<false>(cb, lane) = make_float2(x0, x1);
     }
     __syncthreads();
 
@@ -674,7 +687,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
     for (int p = 0;; ++p) {
       if (is_pts) {
         float xc[J];
-        load_coords(cb, g, xc);
+        load_coords<false>(cb, g, xc);
         float2 dq[KP];
 #pragma unroll
         for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
@@ -756,7 +769,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
           } else {
             x0 = n0;
             x1 = n1;
-            reinterpret_cast<float2*>(cb)[lane] = make_float2(x0, x1);
+            *pub_pair<false>(cb, lane) = make_float2(x0, x1);
           }
         }
         if (lane == 0) *ctl = c;
