@@ -142,11 +142,14 @@ def load_profile_pipes():
         with open(p) as f:
             d = json.load(f)
         return {"fma_pipe_active_pct": d.get("fma_pipe_active_pct"),
-                "issue_active_pct": d.get("issue_active_pct"), "source": d.get("pipe_source"),
+                "issue_active_pct": d.get("issue_active_pct"),
+                "smem_wavefronts_pct": d.get("smem_wavefronts_pct"), "source": d.get("pipe_source"),
                 "note": "frac is algorithmic: 12 flops per (pixel, neighbour, coordinate, sweep) "
                         "as SURVEY.md 8(d) counts Algorithm 1; the low-rank (Gram-form) kernel "
                         "executes about a third of them, so frac can exceed 1 while the FP32 pipe "
-                        "is busy fma_pipe_active_pct of the time"}
+                        "is busy fma_pipe_active_pct of the time; the shared-memory data pipe "
+                        "(tile column loads of the correlation / patch-sum loops) is the co-limit "
+                        "at smem_wavefronts_pct"}
     except Exception:
         return None
 
