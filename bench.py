@@ -148,8 +148,8 @@ def load_profile_pipes():
                         "as SURVEY.md 8(d) counts Algorithm 1; the low-rank (Gram-form) kernel "
                         "executes about a third of them, so frac can exceed 1 while the FP32 pipe "
                         "is busy fma_pipe_active_pct of the time; the shared-memory data pipe "
-                        "(tile column loads of the correlation / patch-sum loops) is the co-limit "
-                        "at smem_wavefronts_pct"}
+                        "(tile column loads of the correlation / patch-sum loops) runs at "
+                        "smem_wavefronts_pct and instruction issue at issue_active_pct: co-limits"}
     except Exception:
         return None
 
