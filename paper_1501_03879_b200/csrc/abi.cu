@@ -49,25 +49,57 @@ const DeviceCaps& device_caps() {
 
 // ---- validation kernels -----------------------------------------------------------
 // code 1: non-finite coordinate, 2: weight non-finite or negative, 3: no positive weight
-__global__ void validate_points_kernel(const float* __restrict__ points,
-                                       const float* __restrict__ weights, int64_t batch, int n,
-                                       int d, unsigned long long* result) {
-  const size_t nd = static_cast<size_t>(n) * d;
+// Weights of each problem (types.hpp:58-68): code 2 for a non-finite or negative weight, 3 when
+// no weight is positive; one block per problem.
+__global__ void validate_weights_kernel(const float* __restrict__ weights, int64_t batch, int n,
+                                        unsigned long long* result) {
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    int bad_pt = 0, bad_w = 0, pos = 0;
-    const float* p = points + b * nd;
-    for (size_t i = threadIdx.x; i < nd; i += blockDim.x) bad_pt |= !isfinite(p[i]);
+    int bad_w = 0, pos = 0;
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
       const float w = weights[b * n + k];
       bad_w |= !(isfinite(w) && w >= 0.0f);
       pos |= w > 0.0f;
     }
-    bad_pt = __syncthreads_or(bad_pt);
     bad_w = __syncthreads_or(bad_w);
     pos = __syncthreads_or(pos);
     if (threadIdx.x == 0) {
-      const int code = bad_pt ? 1 : bad_w ? 2 : !pos ? 3 : 0;
+      const int code = bad_w ? 2 : !pos ? 3 : 0;
       if (code) atomicMin(result, (static_cast<unsigned long long>(b) << 2) | code);
+    }
+  }
+}
+// Coordinates (code 1): one flat HBM-bound scan of all batch * n * d floats with 16-byte loads
+// (four in flight per thread), independent of the problem boundaries; a non-finite element at
+// flat index i reports problem i / nd.  atomicMin over (problem << 2 | code) keeps the lowest
+// problem and, within it, the reference's check order (coordinates, then weights).
+__device__ __forceinline__ void flag_coord(int64_t i, int64_t nd, unsigned long long* result) {
+  atomicMin(result, (static_cast<unsigned long long>(i / nd) << 2) | 1ull);
+}
+__global__ void validate_coords_kernel(const float* __restrict__ points, int64_t total, int64_t nd,
+                                       unsigned long long* result) {
+  const int64_t lead = static_cast<int64_t>(((16 - (reinterpret_cast<uintptr_t>(points) & 15)) & 15) / 4);
+  const int64_t head = lead < total ? lead : total;  // floats before the first 16-byte boundary
+  const int64_t nvec = (total - head) / 4;
+  const float4* __restrict__ body = reinterpret_cast<const float4*>(points + head);
+  const int64_t tid = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  if (tid < head && !isfinite(points[tid])) flag_coord(tid, nd, result);
+  const int64_t tail0 = head + 4 * nvec;
+  if (tid < total - tail0 && !isfinite(points[tail0 + tid])) flag_coord(tail0 + tid, nd, result);
+  constexpr int U = 4;
+  for (int64_t v0 = tid; v0 < nvec; v0 += U * stride) {
+    float4 q[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * stride;
+      q[u] = v < nvec ? __ldcs(body + v) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const float e[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (!isfinite(e[c])) flag_coord(head + 4 * (v0 + u * stride) + c, nd, result);
     }
   }
 }
@@ -84,9 +116,12 @@ __global__ void validate_image_kernel(const float* __restrict__ img, int64_t cou
 
 cudaError_t launch_validate_points(const float* points, const float* weights, int64_t batch, int n,
                                    int d, unsigned long long* result, cudaStream_t stream) {
+  const int64_t nd = static_cast<int64_t>(n) * d, total = batch * nd;
+  const int64_t cgrid = std::max<int64_t>(1, std::min<int64_t>((total / 4 + 255) / 256,
+                                                                device_caps().sms * 8));
+  validate_coords_kernel<<<static_cast<unsigned>(cgrid), 256, 0, stream>>>(points, total, nd, result);
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batch, device_caps().sms * 8));
-  validate_points_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(points, weights, batch, n,
-                                                                          d, result);
+  validate_weights_kernel<<<static_cast<unsigned>(grid), 128, 0, stream>>>(weights, batch, n, result);
   return cudaGetLastError();
 }
 

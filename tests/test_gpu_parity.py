@@ -515,3 +515,45 @@ def test_device_pool_matches_single_device(nb):
             nb.nlem_denoise_multi_host(img, q, devs)
         msgs.append((str(e.value), e.value.iteration, e.value.index))
     assert msgs[0] == msgs[1]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("off", [0, 1, 2, 3])
+def test_point_validation_lowest_problem_misaligned(nb, off):
+    """types.hpp:58-68 through the C ABI on misaligned buffers (odd n*d, offset views): the
+    failure names the LOWEST invalid problem and, within it, the reference's check order
+    (coordinates before weights); the flat 16-byte coordinate scan covers head, body and tail."""
+    import ctypes as C
+    import torch
+    from paper_1501_03879_b200 import _lib as L
+    B, n, d = 37, 13, 7
+    Pbig = torch.rand(B * n * d + 8, device="cuda") * 255
+    Wbig = torch.rand(B * n + 8, device="cuda") + 0.5
+    P = Pbig[off:off + B * n * d]
+    W = Wbig[off:off + B * n]
+    lib = L.load()
+    cfg = L.AdmmConfigC()
+    cfg.mu, cfg.max_iter, cfg.tol_primal = 1.0, 3, 0.0
+    z = torch.empty((B, d), device="cuda")
+
+    def run():
+        f = L.Failure()
+        st = lib.nlem_admm_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d,
+                                   None, nb.BoxConstraint.unconstrained().c(), cfg,
+                                   C.c_void_p(z.data_ptr()), None, None, None, None, C.byref(f),
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        return st, f.message.decode(), int(f.index)
+
+    assert run()[0] == L.NLEM_OK
+    P[(30 * n + 4) * d + 6] = float("nan")                  # problem 30: coordinate
+    P[B * n * d - 1] = float("inf")                         # last element (tail of the scan)
+    st, msg, idx = run()
+    assert st == L.NLEM_INVALID_ARGUMENT and "coordinates must be finite" in msg and idx == 30
+    W[30 * n + 2] = -1.0                                    # same problem: coordinates still first
+    W[12 * n:13 * n] = 0.0                                  # problem 12: no positive weight
+    st, msg, idx = run()
+    assert st == L.NLEM_INVALID_ARGUMENT and "at least one weight must be positive" in msg and idx == 12
+    P[0] = float("-inf")                                    # first element (head of the scan)
+    st, msg, idx = run()
+    assert "coordinates must be finite" in msg and idx == 0
