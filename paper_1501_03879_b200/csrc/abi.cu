@@ -243,6 +243,7 @@ nlem_status validate_params_impl(const nlem_params* p, nlem_failure* f) {
   return check_box(p->range, f);
 }
 
+nlem_status report_invalid(unsigned long long v, nlem_failure* f);
 nlem_status validate_points_dev(const float* points, const float* weights, int64_t batch, int n,
                                 int d, nlem_failure* f, cudaStream_t s) {
   DevSlot slot(s);
@@ -251,6 +252,10 @@ nlem_status validate_points_dev(const float* points, const float* weights, int64
   unsigned long long v = ~0ull;
   if (e == cudaSuccess) e = slot.read(&v);
   if (e != cudaSuccess) return cuda_fail(f, e);
+  return report_invalid(v, f);
+}
+
+nlem_status report_invalid(unsigned long long v, nlem_failure* f) {
   if (v == ~0ull) return NLEM_OK;
   const int code = static_cast<int>(v & 3);
   // types.hpp:58-68 messages
@@ -382,7 +387,18 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
   if (batch == 0) return NLEM_OK;
   if (!points || !weights || !z_out) return invalid(failure, "null buffer");
   if (n * d > (int64_t(1) << 31)) return invalid(failure, "point set too large");
-  if (failure) {
+  AdmmLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), z_init, box,
+               cfg.mu, cfg.max_iter, cfg.tol_primal,
+               res_mode_for(cfg.tol_primal, trace_residual != nullptr), z_out, objective_out,
+               iters_out, trace_objective, trace_residual, nullptr};
+  const bool lr = admm_lr_supported(L);
+  // validation: fused into the low-rank kernel (no extra pass over the points), else separate
+  DevSlot inval(s);
+  if (failure && lr) {
+    const cudaError_t ei = inval.init();
+    if (ei != cudaSuccess) return cuda_fail(failure, ei);
+    L.invalid = inval.ptr;
+  } else if (failure) {
     if (nlem_status st = validate_points_dev(points, weights, batch, static_cast<int>(n),
                                              static_cast<int>(d), failure, s))
       return st;
@@ -390,11 +406,8 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
   DevSlot slot(s);
   cudaError_t e = slot.init();
   if (e != cudaSuccess) return cuda_fail(failure, e);
-  AdmmLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), z_init, box,
-               cfg.mu, cfg.max_iter, cfg.tol_primal,
-               res_mode_for(cfg.tol_primal, trace_residual != nullptr), z_out, objective_out,
-               iters_out, trace_objective, trace_residual, reinterpret_cast<FailureSlot*>(slot.ptr)};
-  if (admm_lr_supported(L)) {
+  L.fail = reinterpret_cast<FailureSlot*>(slot.ptr);
+  if (lr) {
     // low-rank kernel, then the exact p-form kernel over the problems it handed off
     int* scratch = nullptr;  // [0] hand-off count, [1..] hand-off list
     e = cudaMallocAsync(&scratch, (1 + batch) * sizeof(int), s);
@@ -418,6 +431,11 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
   }
   if (e != cudaSuccess) return cuda_fail(failure, e);
   if (!failure) return NLEM_OK;
+  if (L.invalid) {  // an invalid input outranks any numeric failure of the same call
+    unsigned long long iv = ~0ull;
+    if ((e = inval.read(&iv)) != cudaSuccess) return cuda_fail(failure, e);
+    if (nlem_status st = report_invalid(iv, failure)) return st;
+  }
   unsigned long long v = ~0ull;
   if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
   return decode_failure(v, failure, 0);
@@ -436,7 +454,16 @@ nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t
   if (cfg.max_iter < 1) return invalid(failure, "max_iter must be at least 1");
   if (batch == 0) return NLEM_OK;
   if (!points || !weights || !x_out) return invalid(failure, "null buffer");
-  if (failure) {
+  IrlsLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), x_init,
+               cfg.epsilon, cfg.max_iter, cfg.tol, x_out, objective_out, iters_out,
+               trace_objective, nullptr};
+  const bool reg = irls_reg_supported(L);
+  DevSlot inval(s);  // validation fused into the register kernel, else a separate pass
+  if (failure && reg) {
+    const cudaError_t ei = inval.init();
+    if (ei != cudaSuccess) return cuda_fail(failure, ei);
+    L.invalid = inval.ptr;
+  } else if (failure) {
     if (nlem_status st = validate_points_dev(points, weights, batch, static_cast<int>(n),
                                              static_cast<int>(d), failure, s))
       return st;
@@ -444,12 +471,15 @@ nlem_status nlem_irls_batched(const float* points, const float* weights, int64_t
   DevSlot slot(s);
   cudaError_t e = slot.init();
   if (e != cudaSuccess) return cuda_fail(failure, e);
-  IrlsLaunch L{points, weights, batch, static_cast<int>(n), static_cast<int>(d), x_init,
-               cfg.epsilon, cfg.max_iter, cfg.tol, x_out, objective_out, iters_out,
-               trace_objective, reinterpret_cast<FailureSlot*>(slot.ptr)};
-  e = irls_reg_supported(L) ? launch_irls_reg(L, s) : launch_irls_generic(L, s);
+  L.fail = reinterpret_cast<FailureSlot*>(slot.ptr);
+  e = reg ? launch_irls_reg(L, s) : launch_irls_generic(L, s);
   if (e != cudaSuccess) return cuda_fail(failure, e);
   if (!failure) return NLEM_OK;
+  if (L.invalid) {  // an invalid input outranks any numeric failure of the same call
+    unsigned long long iv = ~0ull;
+    if ((e = inval.read(&iv)) != cudaSuccess) return cuda_fail(failure, e);
+    if (nlem_status st = report_invalid(iv, failure)) return st;
+  }
   unsigned long long v = ~0ull;
   if ((e = slot.read(&v)) != cudaSuccess) return cuda_fail(failure, e);
   return decode_failure(v, failure, 0);

@@ -218,6 +218,27 @@ __device__ __forceinline__ float block_sum0(float v, float* scal, int warp, int 
   return t;
 }
 
+// Fused input validation (types.hpp:58-68, the checks validate_points_dev runs as a separate
+// pass): every thread checks the coordinates and weights it loaded (padding slots hold finite 0),
+// the lowest failing (problem << 2 | code) wins; code 1 coordinates, 2 weights, 3 no positive
+// weight - the reference's order within a problem.  One extra barrier per problem.
+__device__ __forceinline__ void check_problem(const float2 (&A)[KP][J], const float2 (&wq)[KP],
+                                              int64_t b, unsigned long long* invalid) {
+  if (invalid == nullptr) return;  // uniform
+  bool bad_pt = false, bad_w = false, pos = false;
+#pragma unroll
+  for (int m = 0; m < KP; ++m) {
+#pragma unroll
+    for (int i = 0; i < J; ++i) bad_pt |= !isfinite(A[m][i].x) || !isfinite(A[m][i].y);
+    bad_w |= !(isfinite(wq[m].x) && wq[m].x >= 0.0f) || !(isfinite(wq[m].y) && wq[m].y >= 0.0f);
+    pos |= wq[m].x > 0.0f || wq[m].y > 0.0f;
+  }
+  const unsigned long long key = static_cast<unsigned long long>(b) << 2;
+  if (bad_pt) atomicMin(invalid, key | 1ull);
+  if (bad_w) atomicMin(invalid, key | 2ull);
+  if (!__syncthreads_or(pos) && threadIdx.x == 0) atomicMin(invalid, key | 3ull);
+}
+
 // Weighted-mean numerator and denominator in one row pass (admm.hpp:40 / irls.hpp:32 with
 // types.hpp:71-74): the point warps write sum_k w_k a_k per coordinate and the weight sum (column
 // 7) into their partial rows; one barrier; the consensus warp divides (sum w a) / (sum w).
@@ -248,7 +269,7 @@ __global__ void __launch_bounds__(ALL, 1)
 admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
                 int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                 int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
-                int* ho_count) {
+                int* ho_count, unsigned long long* invalid) {
   extern __shared__ __align__(16) float smem[];
   float* const stage = smem + SM_STAGE;
   float* const wst = smem + SM_WST;
@@ -322,6 +343,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       }
     }
     const float w_me = real_me ? wv[k_me] : 0.0f;
+    check_problem(A, wq, b, invalid);
     const bool static_eq = !__syncthreads_or(neq);  // every thread is done with the stage
 #ifdef NLEM_BLR_STAMPS
     const long long su_t2 = clock64(); su_load += su_t2 - su_t1;
@@ -609,7 +631,7 @@ __global__ void __launch_bounds__(ALL, 1)
 irls_batched_reg(const float* __restrict__ points, const float* __restrict__ weights,
                  int64_t batch, int n, const float* __restrict__ x_init, float eps, int T,
                  float tol, float* x_out, float* obj_out, int* iters_out, float* tr_obj,
-                 FailureSlot* fail) {
+                 FailureSlot* fail, unsigned long long* invalid) {
   extern __shared__ __align__(16) float smem[];
   float* const stage = smem + SM_STAGE;
   float* const wst = smem + SM_WST;
@@ -657,6 +679,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
       for (int i = 0; i < J; ++i) A[m][i] = make_float2(h0 ? p0[i] : 0.0f, h1 ? p1[i] : 0.0f);
     }
     const float w_me = real_me ? wv[k_me] : 0.0f;
+    check_problem(A, wq, b, invalid);
     __syncthreads();  // every thread is done with the stage
     const int64_t bn = b + gridDim.x;
     if (bn < batch) {
@@ -811,7 +834,7 @@ cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream) {
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.x_init, L.eps, L.max_iter, L.tol, L.x_out, L.obj_out,
-      L.iters_out, L.tr_obj, L.fail);
+      L.iters_out, L.tr_obj, L.fail, L.invalid);
   return cudaGetLastError();
 }
 
@@ -831,7 +854,7 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cud
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
-      L.iters_out, ho_list, ho_count);
+      L.iters_out, ho_list, ho_count, L.invalid);
   return cudaGetLastError();
 }
 

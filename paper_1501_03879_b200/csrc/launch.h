@@ -35,6 +35,9 @@ struct AdmmLaunch {
   float* tr_obj;
   float* tr_res;
   FailureSlot* fail;
+  // fused input validation (types.hpp:58-68) in the batched low-rank kernel: lowest
+  // (problem << 2 | code), ~0 when valid; nullptr = validated separately or not at all
+  unsigned long long* invalid = nullptr;
 };
 
 struct IrlsLaunch {
@@ -51,6 +54,7 @@ struct IrlsLaunch {
   int* iters_out;
   float* tr_obj;
   FailureSlot* fail;
+  unsigned long long* invalid = nullptr;  // fused validation in irls_batched_reg (see AdmmLaunch)
 };
 
 struct NlemDevParams {

@@ -518,30 +518,41 @@ def test_device_pool_matches_single_device(nb):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("off", [0, 1, 2, 3])
-def test_point_validation_lowest_problem_misaligned(nb, off):
+@pytest.mark.parametrize("off", [0, 3])
+@pytest.mark.parametrize("d", [7, 49])
+@pytest.mark.parametrize("solver", ["admm", "irls"])
+def test_point_validation_lowest_problem_misaligned(nb, off, d, solver):
     """types.hpp:58-68 through the C ABI on misaligned buffers (odd n*d, offset views): the
     failure names the LOWEST invalid problem and, within it, the reference's check order
-    (coordinates before weights); the flat 16-byte coordinate scan covers head, body and tail."""
+    (coordinates before weights).  d = 7: the separate flat 16-byte scan (head, body, tail);
+    d = 49: the validation fused into the batched low-rank / register kernels."""
     import ctypes as C
     import torch
     from paper_1501_03879_b200 import _lib as L
-    B, n, d = 37, 13, 7
+    B, n = 37, 13
     Pbig = torch.rand(B * n * d + 8, device="cuda") * 255
     Wbig = torch.rand(B * n + 8, device="cuda") + 0.5
     P = Pbig[off:off + B * n * d]
     W = Wbig[off:off + B * n]
     lib = L.load()
-    cfg = L.AdmmConfigC()
-    cfg.mu, cfg.max_iter, cfg.tol_primal = 1.0, 3, 0.0
     z = torch.empty((B, d), device="cuda")
+    st_ = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def run():
         f = L.Failure()
-        st = lib.nlem_admm_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d,
-                                   None, nb.BoxConstraint.unconstrained().c(), cfg,
-                                   C.c_void_p(z.data_ptr()), None, None, None, None, C.byref(f),
-                                   C.c_void_p(torch.cuda.current_stream().cuda_stream))
+        if solver == "admm":
+            cfg = L.AdmmConfigC()
+            cfg.mu, cfg.max_iter, cfg.tol_primal = 1.0, 3, 0.0
+            st = lib.nlem_admm_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d,
+                                       None, nb.BoxConstraint.unconstrained().c(), cfg,
+                                       C.c_void_p(z.data_ptr()), None, None, None, None,
+                                       C.byref(f), st_)
+        else:
+            cfg = L.IrlsConfigC()
+            cfg.epsilon, cfg.max_iter, cfg.tol = 1e-4, 3, -1.0
+            st = lib.nlem_irls_batched(C.c_void_p(P.data_ptr()), C.c_void_p(W.data_ptr()), B, n, d,
+                                       None, cfg, C.c_void_p(z.data_ptr()), None, None, None,
+                                       C.byref(f), st_)
         torch.cuda.synchronize()
         return st, f.message.decode(), int(f.index)
 
@@ -554,6 +565,9 @@ def test_point_validation_lowest_problem_misaligned(nb, off):
     W[12 * n:13 * n] = 0.0                                  # problem 12: no positive weight
     st, msg, idx = run()
     assert st == L.NLEM_INVALID_ARGUMENT and "at least one weight must be positive" in msg and idx == 12
+    W[5 * n + 12] = float("nan")                            # problem 5: non-finite weight
+    st, msg, idx = run()
+    assert "weights must be finite and nonnegative" in msg and idx == 5
     P[0] = float("-inf")                                    # first element (head of the scan)
     st, msg, idx = run()
     assert "coordinates must be finite" in msg and idx == 0
