@@ -703,6 +703,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         for (int q = 0; q < R; ++q) vac2[q] = make_float2(0.0f, 0.0f);
         float2 us2 = make_float2(0.0f, 0.0f);
         const float2 one2 = make_float2(1.0f, 1.0f);
+        // non-finite ||p||^2 test (admm.hpp:67-68 via the norm): N * 0 summed over the points is 0
+        // unless some N is inf / NaN.  Points with lambda = 0 are included: their N can only turn
+        // non-finite through the shared c~ / Gram values, which makes the self point's N (lambda
+        // = 1/mu != 0) non-finite in the same sweep, so the flagged sweep is the reference's.
+        float2 nchk = make_float2(0.0f, 0.0f);
         static_for<SEGL>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           // point i of both slots as one register pair per field
@@ -722,7 +727,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           float2 sc, Nc;
           {
             const float lx = lm[2 * i], ly = lm[2 * i + 1];
-            fnorm |= (lx != 0.0f && !isfinite(N.x)) || (ly != 0.0f && !isfinite(N.y));
+            nchk = __ffma2_rn(N, make_float2(0.0f, 0.0f), nchk);
             Nc = make_float2(fmaxf(N.x, 0.0f), fmaxf(N.y, 0.0f));
             sc.x = lx != 0.0f ? fminf(1.0f, lx * rsq(Nc.x)) : 0.0f;
             sc.y = ly != 0.0f ? fminf(1.0f, ly * rsq(Nc.y)) : 0.0f;
@@ -768,6 +773,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
         usum = us2.x + us2.y;
+        fnorm = !isfinite(nchk.x + nchk.y);
       }
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
       float gA, gB, xs[5];
