@@ -731,8 +731,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
             Nc = make_float2(fmaxf(N.x, 0.0f), fmaxf(N.y, 0.0f));
             sc.x = lx != 0.0f ? fminf(1.0f, lx * rsq(Nc.x)) : 0.0f;
             sc.y = ly != 0.0f ? fminf(1.0f, ly * rsq(Nc.y)) : 0.0f;
-            sne1 |= (((realmask >> i) & 1u) && sc.x != 1.0f) ||
-                    (((realmask >> (SEGL + i)) & 1u) && sc.y != 1.0f);
           }
           const float2 B = __fadd2_rn(K, D_);
           const float2 ev = __fmul2_rn(sc, al3);
@@ -774,6 +772,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
         usum = us2.x + us2.y;
         fnorm = !isfinite(nchk.x + nchk.y);
+        if (static_eq) {  // warp-uniform and rare: only an all-equal footprint can stop exactly;
+          // the prox scales were just stored as al0 (fields 8 / 9 of each point pair) - reread
+          // them from TMEM instead of testing every point in the sweep
+          tm_wait_st();
+          static_for<SEGL>([&](auto ic) {
+            constexpr int i = decltype(ic)::value;
+            float st[16];
+            tm_ld16c_wait<i * 2 * NF>(tw, st);
+            sne1 |= (((realmask >> i) & 1u) && st[8] != 1.0f) ||
+                    (((realmask >> (SEGL + i)) & 1u) && st[9] != 1.0f);
+          });
+        }
       }
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
       float gA, gB, xs[5];
