@@ -154,8 +154,22 @@ def load_profile_pipes():
         return None
 
 
+def bench_config(gpus: int) -> dict:
+    """The workload description, identical in both arms (the driver compares them)."""
+    return {"workload": "BASELINE config 3: NLEM denoise 4096x4096 synthetic, k=7 (d=49), "
+                        "S=21 (n<=441), h=10*sigma (h_ref=2100), box [0,255], mu=1, NLM init, "
+                        "T=10 ADMM sweeps",
+            "rows": CFG["rows"], "cols": CFG["cols"], "sigma": CFG["sigma"], "patch": 7,
+            "search": 21, "iters": CFG["iters"], "parallelism": f"row-bands x{gpus}",
+            "halo_rows": 13,
+            "l2": "GPU arm: 256 MiB buffer written between timed steps (L2 flushed); CPU arm: n/a"}
+
+
 def cpu_reference(noisy, params_kw, sample_rows, threads):
-    """Time the FP64 oracle (restated reference) on a row sample; returns (Mpix/s, seconds)."""
+    """Time the FP64 oracle (restated reference) on a row sample.
+
+    Returns (Mpix/s, seconds, pixels, rows {r: float64 row}) — the rows double as the parity
+    reference of the GPU output on the same sample."""
     from oracle import oracle as O
 
     o = O.make_params(search=params_kw["search"], patch=params_kw["patch"], h=params_kw["h"],
@@ -164,11 +178,63 @@ def cpu_reference(noisy, params_kw, sample_rows, threads):
     X = noisy.astype(np.float64)
     t0 = time.perf_counter()
     px = 0
+    got = {}
     for r in sample_rows:
-        O.nlem_denoise(X, o, rows=(r, r + 1))
+        got[r] = O.nlem_denoise(X, o, rows=(r, r + 1))[r]
         px += X.shape[1]
     dt = time.perf_counter() - t0
-    return px / dt / 1e6, dt, px
+    return px / dt / 1e6, dt, px, got
+
+
+def parity_rows(rows: int, world: int):
+    """Oracle sample of the config-3 image: the top and bottom 4 rows (clipped windows, mirrored
+    patches), 32 interior rows at stride 128 and, at N > 1, the two rows either side of every
+    band boundary (halo exchange by overlapping reads)."""
+    s = set(range(4)) | set(range(rows - 4, rows)) | set(range(37, rows, 128))
+    if world > 1:
+        per = (rows + world - 1) // world
+        for b in range(1, world):
+            s |= {b * per - 2, b * per - 1, b * per, b * per + 1}
+    return sorted(r for r in s if 0 <= r < rows)
+
+
+def reference_arm(args, rank, config, h_ref, threads):
+    """--impl reference: the reference algorithm (FP64 oracle restatement; the reference needs
+    Eigen, absent) on the host cores.  Inputs come from the oracle-side generator
+    (oracle/synth_oracle.cpp, bitwise equal to the product's), so this arm never loads the
+    product library."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    _, noisy = O.synth_config_image(3)
+    pkw = dict(search=21, patch=7, h=h_ref, iters=CFG["iters"], mu=CFG["mu"])
+    rows_per_step = 8
+    all_rows = list(range(0, CFG["rows"], 7))  # deterministic stride over the whole image
+    samples = [all_rows[i * rows_per_step:(i + 1) * rows_per_step]
+               for i in range(args.warmup + args.steps)]
+    for smp in samples[: args.warmup]:
+        cpu_reference(noisy, pkw, smp, threads)
+    secs, pxs = 0.0, 0
+    for smp in samples[args.warmup:]:
+        _, dt, px, _ = cpu_reference(noisy, pkw, smp, threads)
+        secs += dt
+        pxs += px
+    value = pxs / secs / 1e6
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixels/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config,
+            "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": threads,
+                             "kind": "port",
+                             "sample": f"{rows_per_step} full rows ({rows_per_step}x4096 px) of the "
+                                       "config-3 image per step (rows 0, 7, 14, ...), FP64 oracle "
+                                       "restatement of the reference with its parallel_for over "
+                                       "pixels (Eigen absent: reference unbuildable)"},
+            "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -192,44 +258,10 @@ def main():
 
     from paper_1501_03879_b200 import synth
 
-    config = {"workload": "BASELINE config 3: NLEM denoise 4096x4096 synthetic, k=7 (d=49), "
-                          "S=21 (n<=441), h=10*sigma (h_ref=2100), box [0,255], mu=1, NLM init, "
-                          "T=10 ADMM sweeps",
-              "rows": CFG["rows"], "cols": CFG["cols"], "sigma": CFG["sigma"], "patch": 7,
-              "search": 21, "iters": CFG["iters"], "parallelism": f"row-bands x{args.gpus}",
-              "halo_rows": 13}
+    config = bench_config(args.gpus)
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        _, noisy = synth.config_image(3)
-        pkw = dict(search=21, patch=7, h=h_ref, iters=CFG["iters"], mu=CFG["mu"])
-        rows_per_step = 2
-        rng = np.random.default_rng(0)
-        samples = [sorted(rng.choice(CFG["rows"], rows_per_step, replace=False).tolist())
-                   for _ in range(args.warmup + args.steps)]
-        for s in samples[: args.warmup]:
-            cpu_reference(noisy, pkw, s, threads)
-        vals, secs, pxs = [], 0.0, 0
-        for s in samples[args.warmup:]:
-            v, dt, px = cpu_reference(noisy, pkw, s, threads)
-            vals.append(v)
-            secs += dt
-            pxs += px
-        value = pxs / secs / 1e6
-        line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixels/s",
-                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": config,
-                "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": threads,
-                                 "kind": "port",
-                                 "sample": f"{rows_per_step} random full rows (2x4096 px) of the "
-                                           "config-3 image per step, FP64 oracle restatement of "
-                                           "the reference (Eigen absent: reference unbuildable)"},
-                "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
-                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
+        reference_arm(args, rank, config, h_ref, threads)
         return
 
     import torch
@@ -348,15 +380,43 @@ def main():
     psnr_noisy = 10 * math.log10(255 ** 2 / float(np.mean((noisy.astype(np.float64) - clean) ** 2)))
     psnr_out = 10 * math.log10(255 ** 2 / float(np.mean((full.astype(np.float64) - clean) ** 2)))
 
-    cpu = None
-    if world == 1 and not args.no_cpu_baseline:
-        rng = np.random.default_rng(1)
-        sample = sorted(rng.choice(rows, args.cpu_sample_rows, replace=False).tolist())
-        v, dt, px = cpu_reference(noisy, dict(search=21, patch=7, h=h_ref, iters=CFG["iters"],
-                                              mu=CFG["mu"]), sample, threads)
-        cpu = {"value": v, "unit": "Mpixels/s", "cores": threads, "kind": "port",
-               "sample": f"{len(sample)} random full rows ({px} px) of the config-3 image, FP64 "
-                         f"oracle restatement, {dt:.1f} s"}
+    # ---- oracle rows of the same image: CPU baseline (N = 1) and parity of the GPU output
+    cpu, parity = None, None
+    if not args.no_cpu_baseline:
+        pkw = dict(search=21, patch=7, h=h_ref, iters=CFG["iters"], mu=CFG["mu"])
+        prow = parity_rows(rows, world)
+        # timed CPU baseline on the interior rows (full 441-point windows, like the bulk of
+        # the image); the edge rows are oracle-computed for parity only
+        inner = [r for r in prow if 10 <= r < rows - 10]
+        v, dt, px, ref_rows = cpu_reference(noisy, pkw, inner, threads)
+        ref_rows.update(cpu_reference(noisy, pkw, [r for r in prow if r not in ref_rows], threads)[3])
+        sel = np.array(prow)
+        gpu_rows = full[sel].astype(np.float64)
+        ora_rows = np.stack([ref_rows[r] for r in prow])
+        clean_rows = clean[sel].astype(np.float64)
+
+        def psnr(a):
+            return 10 * math.log10(255 ** 2 / float(np.mean((a - clean_rows) ** 2)))
+
+        max_abs = float(np.abs(gpu_rows - ora_rows).max())
+        dpsnr = abs(psnr(gpu_rows) - psnr(ora_rows))
+        parity = {"rows": len(prow), "pixels": len(prow) * cols, "max_abs_diff": max_abs,
+                  "psnr_gpu_db": psnr(gpu_rows), "psnr_oracle_db": psnr(ora_rows),
+                  "dpsnr_rows_db": dpsnr, "tol_abs": 1e-2, "tol_dpsnr_db": 0.01,
+                  "ok": bool(max_abs <= 1e-2 and dpsnr <= 0.01),
+                  "sample": "rows 0-3, 4092-4095, 37 + 128 i" +
+                            (", +-2 rows at every band boundary" if world > 1 else "") +
+                            "; FP64 oracle on the same float32 input"}
+        if world == 1:
+            one = inner[len(inner) // 2]
+            v1, dt1, px1, _ = cpu_reference(noisy, pkw, [one], 1)
+            cpu = {"value": v, "unit": "Mpixels/s", "cores": threads, "kind": "port",
+                   "sample": f"{len(inner)} full interior rows ({px} px, {100.0 * px / (rows * cols):.2f}% "
+                             f"of the config-3 image: rows 37 + 128 i), FP64 oracle "
+                             f"restatement with the reference's parallel_for over pixels on "
+                             f"{threads} threads, {dt:.1f} s",
+                   "single_thread": {"value": v1, "unit": "Mpixels/s", "cores": 1,
+                                     "sample": f"row {one} ({px1} px), {dt1:.1f} s"}}
 
     secondary = None
     if world == 1 and not args.no_secondary:
@@ -376,7 +436,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded generator of BASELINE.json config 3, SURVEY.md §8d)",
-        "config": dict(config, l2="flushed between steps (256 MiB write)"),
+        "config": config,
         "roofline": {"bound": "fp32", "achieved": float(achieved_t.item()), "peak": peak,
                      "unit": "TFLOP/s", "frac": float(achieved_t.item()) / peak,
                      "traffic": load_profile_traffic(),
@@ -390,11 +450,14 @@ def main():
                                                 if clk.get("sm_mhz") and clk.get("sm_max_mhz")
                                                 else None)},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": {"value": e2e_val, "unit": "Mpixels/s",
                 "h2d_bytes_per_step": int(band_in.nbytes), "d2h_bytes_per_step": int(nrows * cols * 4),
                 "entry": "nlem_denoise_rows_host (C-ABI, pinned host buffers)"},
         "clocks": clk,
-        "gpu_launches": 3 * args.steps,  # pad + low-rank pixel kernel + tile kernel over its hand-off list
+        # per step: validate_image_kernel + pad_band_kernel + nlem_pixels_lr + nlem_pixels_tile over
+        # its hand-off list (profiles/r2_launches_bench.txt)
+        "gpu_launches": 4 * args.steps,
         "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
         "secondary": secondary,
         "step_ms": [round(x, 2) for x in step_ms],
@@ -403,6 +466,8 @@ def main():
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        sys.exit("parity breach on the config-3 oracle rows: " + json.dumps(parity))
 
 
 if __name__ == "__main__":

@@ -215,6 +215,34 @@ nlem_status nlem_optimality_residual_batched(const float* points, const float* w
                                              const float* z, float* residual_out,
                                              nlem_failure* failure, void* stream);
 
+/* build_patch_stack(image, row, col, search, k, h) (proj/include/nlem/patch.hpp:48-49,
+ * proj/src/patch.cpp:90-114) for one pixel, from a HOST image on `device`: the clipped search
+ * window in row-major neighbour order, each neighbour's k x k mirrored patch
+ * (patch.cpp:9-38) at patches_out[j*k*k ..], weights exp(-||P_j - P_self||^2 / h^2) with the
+ * self weight exactly 1 (patch.cpp:52-61).  patches_out [search*search][k*k] and weights_out
+ * [search*search] are host buffers sized for the unclipped window; *n_out receives the
+ * neighbour count n and *self_column_out the index of the pixel itself.  Reference messages
+ * for invalid input (validate_image, "... must be odd and positive", "pixel outside the
+ * image", "similarity bandwidth h must be positive"). */
+nlem_status nlem_patch_stack_host(const float* image, int64_t rows, int64_t cols, int64_t row,
+                                  int64_t col, int32_t search, int32_t patch, float h,
+                                  float* patches_out, float* weights_out, int64_t* n_out,
+                                  int64_t* self_column_out, nlem_failure* failure,
+                                  int32_t device);
+
+/* solve_patch(stack, params) (proj/include/nlem/nlem.hpp:60-62, proj/src/nlem.cpp:20-56) on
+ * `device`, from host buffers: patches [n][d] (point-contiguous), weights [n], self_column.
+ * init_out [d] receives the initial patch (nlem.cpp:13-18, params->init_mode), patch_out [d]
+ * the solved patch inside params->range: ADMM from init (max_iter = solver_iters, tol 0),
+ * IRLS from init (epsilon, tol = irls_tol) then clipped, or NlmOnly = the clipped weighted
+ * mean.  The per-iteration callback of the reference cannot cross the ABI (use
+ * nlem_denoise's frames).  Errors as the solvers': INVALID_ARGUMENT with the reference
+ * message ("patch stack has no valid self column", validate(NlemParams), types.hpp:58-68),
+ * NUMERIC_FAILURE with the iteration. */
+nlem_status nlem_solve_patch_host(const float* patches, const float* weights, int64_t n, int64_t d,
+                                  int64_t self_column, const nlem_params* params, float* init_out,
+                                  float* patch_out, nlem_failure* failure, int32_t device);
+
 /* Halo (rows) a band needs on each side: S/2 + k/2 (13 for S=21, k=7). */
 int64_t nlem_band_halo(const nlem_params* params);
 

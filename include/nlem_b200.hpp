@@ -251,6 +251,80 @@ inline std::vector<Image> nlem_denoise_snapshots(const Image& noisy, const NlemP
   return res;
 }
 
+// proj/src/patch.cpp:9-16: whole-sample reflection (..., 2, 1, 0, 1, 2, ...), period 2 (n - 1)
+inline int64_t mirror_index(int64_t i, int64_t n) {
+  if (n < 1) throw std::invalid_argument("mirror_index needs a non-empty axis");
+  if (n == 1) return 0;
+  const int64_t period = 2 * (n - 1);
+  const int64_t m = ((i % period) + period) % period;
+  return m < n ? m : period - m;
+}
+
+// proj/include/nlem/patch.hpp:33-37 (patches d x n column-major == [n][d] row-major)
+struct PatchStack {
+  std::vector<float> patches;
+  std::vector<float> weights;
+  int64_t d = 0;
+  int64_t self_column = -1;
+  int64_t size() const { return d ? static_cast<int64_t>(patches.size()) / d : 0; }
+};
+
+// proj/include/nlem/nlem.hpp:52-55
+struct PatchSolve {
+  std::vector<float> init;
+  std::vector<float> patch;
+};
+
+// proj/src/patch.cpp:90-114 — one pixel's stack (gathered on `device`)
+inline PatchStack build_patch_stack(const Image& image, int64_t row, int64_t col, int search, int k,
+                                    double h, int device = 0) {
+  PatchStack s;
+  s.d = static_cast<int64_t>(k) * k;
+  const int64_t cap = static_cast<int64_t>(search > 0 ? search : 0) * (search > 0 ? search : 0);
+  s.patches.resize(static_cast<size_t>(cap * s.d));
+  s.weights.resize(static_cast<size_t>(cap));
+  int64_t n = 0;
+  nlem_failure f;
+  detail::raise(nlem_patch_stack_host(image.data(), image.rows(), image.cols(), row, col, search, k,
+                                      static_cast<float>(h), s.patches.data(), s.weights.data(), &n,
+                                      &s.self_column, &f, device),
+                f);
+  s.patches.resize(static_cast<size_t>(n * s.d));
+  s.weights.resize(static_cast<size_t>(n));
+  return s;
+}
+
+// proj/src/nlem.cpp:13-18 (the self patch, or points * (w / sum w)), computed on `device`
+inline std::vector<float> initial_patch(const PatchStack& stack, PatchInit mode, int device = 0);
+
+// proj/include/nlem/nlem.hpp:60-62, proj/src/nlem.cpp:20-56: the initial patch and the solved
+// patch (inside params.range) of one stack.  The reference's on_iterate callback cannot cross
+// the ABI; nlem_denoise_snapshots gives the per-iteration centre values of whole images.
+inline PatchSolve solve_patch(const PatchStack& stack, const NlemParams& params, int device = 0) {
+  if (stack.weights.size() != static_cast<size_t>(stack.size()))
+    throw std::invalid_argument("weight count does not match point count");
+  PatchSolve r;
+  r.init.resize(static_cast<size_t>(stack.d));
+  r.patch.resize(static_cast<size_t>(stack.d));
+  const nlem_params p = params.c();
+  nlem_failure f;
+  detail::raise(nlem_solve_patch_host(stack.patches.data(), stack.weights.data(), stack.size(),
+                                      stack.d, stack.self_column, &p, r.init.data(), r.patch.data(),
+                                      &f, device),
+                f);
+  return r;
+}
+
+inline std::vector<float> initial_patch(const PatchStack& stack, PatchInit mode, int device) {
+  NlemParams p;  // NlmOnly: no solve beyond the weighted mean; init_mode picks the init
+  p.search = p.patch = 1;
+  p.h = 1.0;
+  p.solver = DenoiseSolver::NlmOnly;
+  p.init_mode = mode;
+  p.range = BoxConstraint::unconstrained();
+  return solve_patch(stack, p, device).init;
+}
+
 // proj/src/nlm.cpp:31-51 (host staging through torch-free C-ABI: device path only exists
 // as nlm_denoise(device buffers); here stage via the NlmOnly solver of nlem_denoise_host,
 // which computes the same centre coordinate of the weighted-mean patch)

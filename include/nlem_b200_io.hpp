@@ -331,66 +331,4 @@ inline Image add_gaussian_noise(const Image& clean, double sigma, uint64_t seed)
   return out;
 }
 
-// ------------------------------------------------------------------ one pixel's patch stack
-inline int64_t mirror_index(int64_t i, int64_t n) {  // patch.cpp:9-16
-  if (n < 1) throw std::invalid_argument("mirror_index needs a non-empty axis");
-  if (n == 1) return 0;
-  const int64_t period = 2 * (n - 1);
-  int64_t m = i % period;
-  if (m < 0) m += period;
-  return m < n ? m : period - m;
-}
-
-struct PatchStack {  // patch.hpp:33-37 ([n][d] points, clipped-window row-major order)
-  PointSet points;
-  int64_t self_column = 0;
-};
-
-inline PatchStack build_patch_stack(const Image& img, int64_t row, int64_t col, int search, int k,
-                                    double h) {
-  const int64_t hs = search / 2, hk = k / 2, d = static_cast<int64_t>(k) * k;
-  const int64_t r0 = std::max<int64_t>(0, row - hs), r1 = std::min<int64_t>(img.rows() - 1, row + hs);
-  const int64_t c0 = std::max<int64_t>(0, col - hs), c1 = std::min<int64_t>(img.cols() - 1, col + hs);
-  PatchStack st;
-  st.points.d = d;
-  for (int64_t r = r0; r <= r1; ++r)
-    for (int64_t c = c0; c <= c1; ++c) {
-      if (r == row && c == col) st.self_column = st.points.size();
-      for (int64_t dr = -hk; dr <= hk; ++dr)
-        for (int64_t dc = -hk; dc <= hk; ++dc)
-          st.points.points.push_back(img(mirror_index(r + dr, img.rows()), mirror_index(c + dc, img.cols())));
-    }
-  const int64_t n = st.points.size();
-  const double inv_h2 = 1.0 / (h * h);
-  const float* self = &st.points.points[st.self_column * d];
-  for (int64_t j = 0; j < n; ++j) {  // patch.cpp:52-61
-    double s = 0.0;
-    for (int64_t i = 0; i < d; ++i) {
-      const double e = static_cast<double>(st.points.points[j * d + i]) - self[i];
-      s += e * e;
-    }
-    st.points.weights.push_back(static_cast<float>(std::exp(-s * inv_h2)));
-  }
-  return st;
-}
-
-// nlem.cpp:13-18: noisy = the self patch, nlm = points * (w / sum w)
-inline std::vector<float> initial_patch(const PatchStack& st, PatchInit mode) {
-  const int64_t d = st.points.dim(), n = st.points.size();
-  std::vector<float> z(static_cast<size_t>(d), 0.0f);
-  if (mode == PatchInit::NoisyPatch) {
-    for (int64_t i = 0; i < d; ++i) z[i] = st.points.points[st.self_column * d + i];
-    return z;
-  }
-  double wsum = 0.0;
-  for (float w : st.points.weights) wsum += w;
-  std::vector<double> acc(static_cast<size_t>(d), 0.0);
-  for (int64_t k = 0; k < n; ++k) {
-    const double c = st.points.weights[k] / wsum;
-    for (int64_t i = 0; i < d; ++i) acc[i] += st.points.points[k * d + i] * c;
-  }
-  for (int64_t i = 0; i < d; ++i) z[i] = static_cast<float>(acc[i]);
-  return z;
-}
-
 }  // namespace nlem

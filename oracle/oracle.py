@@ -62,8 +62,9 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        if not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(
-            os.path.join(_HERE, "nlem_oracle.cpp")
+        srcs = ("nlem_oracle.cpp", "synth_oracle.cpp")
+        if not os.path.exists(_SO) or any(
+            os.path.getmtime(_SO) < os.path.getmtime(os.path.join(_HERE, f)) for f in srcs
         ):
             build()
         L = C.CDLL(_SO)
@@ -100,6 +101,11 @@ def lib():
         L.oracle_optimality_residual.restype = C.c_double
         L.oracle_optimality_residual.argtypes = [
             _dp, _dp, C.c_int64, C.c_int64, C.c_int32, C.c_double, C.c_double, _dp]
+        L.oracle_synth_noisy_image.argtypes = [
+            C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_uint64,
+            C.c_void_p, C.c_void_p]
+        L.oracle_synth_point_sets.argtypes = [
+            C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_int64, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -316,3 +322,34 @@ def optimality_residual(points, weights, z, box=None):
     bounded, lo, hi = (1, box[0], box[1]) if box is not None else (0, 0.0, 0.0)
     return lib().oracle_optimality_residual(pp, pw, points.shape[0], points.shape[1], bounded,
                                             lo, hi, pz)
+
+
+# ---- seeded inputs, independent of the product library (oracle/synth_oracle.cpp)
+SYNTH_CONFIGS = {
+    0: dict(rows=128, cols=128, rects=12, disks=8, sigma=20.0),
+    2: dict(rows=512, cols=512, rects=40, disks=30, sigma=20.0),
+    3: dict(rows=4096, cols=4096, rects=2000, disks=1500, sigma=30.0),
+}
+
+
+def synth_noisy_image(rows, cols, rects, disks, sigma, image_seed=0, noise_seed=1):
+    """(clean, noisy) float32 images of the BASELINE.json generator."""
+    clean = np.empty((rows, cols), np.float32)
+    noisy = np.empty((rows, cols), np.float32)
+    lib().oracle_synth_noisy_image(rows, cols, rects, disks, float(sigma), image_seed, noise_seed,
+                                   clean.ctypes.data, noisy.ctypes.data)
+    return clean, noisy
+
+
+def synth_config_image(cfg: int, **over):
+    c = dict(SYNTH_CONFIGS[cfg])
+    c.update(over)
+    return synth_noisy_image(c["rows"], c["cols"], c["rects"], c["disks"], c["sigma"])
+
+
+def synth_point_sets(batch, n=441, d=49, seed_base=1000, first=0):
+    """Config-1 point sets: (points [B][n][d], weights [B][n]) float32."""
+    pts = np.empty((batch, n, d), np.float32)
+    w = np.empty((batch, n), np.float32)
+    lib().oracle_synth_point_sets(batch, n, d, seed_base, first, pts.ctypes.data, w.ctypes.data)
+    return pts, w

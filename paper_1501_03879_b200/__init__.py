@@ -7,7 +7,8 @@ the CUDA library or a GPU is missing.
 """
 from .api import (  # noqa: F401
     AdmmConfig, BoxConstraint, CudaError, InvalidArgument, IrlsConfig, NlemParams,
-    NumericFailure, SolverResult, TraceRecord, admm_euclidean_median, band_halo,
+    NumericFailure, PatchSolve, PatchStack, SolverResult, TraceRecord, admm_euclidean_median,
+    band_halo, build_patch_stack, solve_patch,
     default_init_mode, frames_psnr, optimality_residual, irls_euclidean_median, nlem_denoise, nlem_denoise_host,
     nlem_denoise_multi_host,
     nlem_denoise_rows, nlem_denoise_rows_host, nlem_denoise_snapshots, nlm_denoise, validate,

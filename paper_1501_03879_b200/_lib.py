@@ -55,6 +55,7 @@ EXPORTS = [
     "nlm_denoise", "nlem_band_halo",
     "nlem_add_gaussian_noise", "nlem_synth_clean_image", "nlem_synth_noisy_image",
     "nlem_synth_point_sets", "nlem_frames_psnr", "nlem_optimality_residual_batched",
+    "nlem_patch_stack_host", "nlem_solve_patch_host",
 ]
 
 _lib = None
@@ -108,6 +109,11 @@ def load(build_if_missing: bool = True):
     L.nlem_frames_psnr.argtypes = [vp, vp, C.c_int64, C.c_int64, vp, C.POINTER(Failure), vp]
     L.nlem_optimality_residual_batched.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int64, Box, vp,
                                                    vp, C.POINTER(Failure), vp]
+    L.nlem_patch_stack_host.argtypes = [vp, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                        C.c_int32, C.c_float, vp, vp, C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64), C.POINTER(Failure), C.c_int32]
+    L.nlem_solve_patch_host.argtypes = [vp, vp, C.c_int64, C.c_int64, C.c_int64, C.POINTER(ParamsC),
+                                        vp, vp, C.POINTER(Failure), C.c_int32]
     L.nlem_add_gaussian_noise.argtypes = [vp, C.c_int64, C.c_double, C.c_uint64, vp]
     L.nlem_synth_clean_image.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_uint64, vp]
     L.nlem_synth_noisy_image.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_double,

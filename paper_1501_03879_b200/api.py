@@ -344,12 +344,22 @@ def nlm_denoise(noisy, params: NlemParams):
     return _image_call(noisy, params, False, "nlm")[0]
 
 
+def _host_out(out, shape):
+    """A caller-supplied host output buffer must be a C-contiguous float32 array of `shape`
+    (the C-ABI writes rows*cols floats through its pointer)."""
+    if out is None:
+        return np.empty(shape, np.float32)
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float32 and out.flags.c_contiguous
+            and out.shape == tuple(shape) and out.flags.writeable):
+        raise InvalidArgument(f"out must be a writeable C-contiguous float32 array of shape {tuple(shape)}")
+    return out
+
+
 def nlem_denoise_host(noisy: np.ndarray, params: NlemParams, out: np.ndarray | None = None,
                       device: int = 0) -> np.ndarray:
     """Host-buffer entry (nlem_denoise_host): H2D, kernels and D2H inside the call."""
     noisy = np.ascontiguousarray(noisy, dtype=np.float32)
-    if out is None:
-        out = np.empty_like(noisy)
+    out = _host_out(out, noisy.shape)
     f = L.Failure()
     st = L.load().nlem_denoise_host(noisy.ctypes.data, noisy.shape[0], noisy.shape[1],
                                     C.byref(params.c()), out.ctypes.data, None, C.byref(f), device)
@@ -379,14 +389,66 @@ def nlem_denoise_rows_host(noisy_rows: np.ndarray, in_row0: int, rows: int, cols
                            out: np.ndarray | None = None, device: int = 0) -> np.ndarray:
     """Host-buffer row band (nlem_denoise_rows_host): H2D, kernels and D2H inside the call."""
     noisy_rows = np.ascontiguousarray(noisy_rows, dtype=np.float32)
-    if out is None:
-        out = np.empty((out_rows, cols), np.float32)
+    if noisy_rows.ndim != 2 or noisy_rows.shape[1] != cols:
+        raise InvalidArgument("input rows must be [in_rows][cols]")
+    out = _host_out(out, (out_rows, cols))
     f = L.Failure()
     st = L.load().nlem_denoise_rows_host(noisy_rows.ctypes.data, in_row0, noisy_rows.shape[0],
                                          rows, cols, out_row0, out_rows, C.byref(params.c()),
                                          out.ctypes.data, None, C.byref(f), device)
     _raise(st, f)
     return out
+
+
+@dataclass
+class PatchStack:
+    """proj/include/nlem/patch.hpp:33-37 (patches [n][d] point-contiguous = Eigen d x n)."""
+
+    patches: np.ndarray
+    weights: np.ndarray
+    self_column: int = -1
+
+
+@dataclass
+class PatchSolve:
+    """proj/include/nlem/nlem.hpp:52-55."""
+
+    init: np.ndarray
+    patch: np.ndarray
+
+
+def build_patch_stack(image: np.ndarray, row: int, col: int, search: int, k: int, h: float,
+                      device: int = 0) -> PatchStack:
+    """proj/src/patch.cpp:90-114 for one pixel of a host image (gathered on the GPU)."""
+    image = np.ascontiguousarray(image, dtype=np.float32)
+    if image.ndim != 2:
+        raise InvalidArgument("image must be non-empty")
+    pts = np.empty((search * search, k * k), np.float32)
+    w = np.empty(search * search, np.float32)
+    n, sc = C.c_int64(), C.c_int64()
+    f = L.Failure()
+    st = L.load().nlem_patch_stack_host(image.ctypes.data, image.shape[0], image.shape[1], row, col,
+                                        search, k, h, pts.ctypes.data, w.ctypes.data, C.byref(n),
+                                        C.byref(sc), C.byref(f), device)
+    _raise(st, f)
+    return PatchStack(pts[: n.value].copy(), w[: n.value].copy(), int(sc.value))
+
+
+def solve_patch(stack: PatchStack, params: NlemParams, device: int = 0) -> PatchSolve:
+    """proj/src/nlem.cpp:20-56 (init + ADMM / IRLS-then-clip / NlmOnly) on the GPU."""
+    P = np.ascontiguousarray(stack.patches, dtype=np.float32)
+    W = np.ascontiguousarray(stack.weights, dtype=np.float32)
+    if P.ndim != 2 or W.shape != (P.shape[0],):
+        raise InvalidArgument("weight count does not match point count")
+    n, d = P.shape
+    init = np.empty(d, np.float32)
+    patch = np.empty(d, np.float32)
+    f = L.Failure()
+    st = L.load().nlem_solve_patch_host(P.ctypes.data, W.ctypes.data, n, d, stack.self_column,
+                                        C.byref(params.c()), init.ctypes.data, patch.ctypes.data,
+                                        C.byref(f), device)
+    _raise(st, f)
+    return PatchSolve(init, patch)
 
 
 def band_halo(params: NlemParams) -> int:

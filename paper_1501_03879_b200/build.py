@@ -17,8 +17,7 @@ SO = os.path.join(OUT_DIR, "libnlem_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu",
-              "kernels_nlem_seg2.cu", "kernels_nlem_lr.cu", "kernels_batched_lr.cu",
-              "kernels_aux.cu"]
+              "kernels_nlem_lr.cu", "kernels_batched_lr.cu", "kernels_aux.cu"]
 CXX_SOURCES = ["synth.cpp", "multi_host.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -79,11 +78,19 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     if not force and not variant and not _stale():
         return SO
     os.makedirs(OUT_DIR, exist_ok=True)
-    extra = [_VARIANT_TOKENS[t] for t in variant.split("_") if t]
+    toks = [t for t in variant.split("_") if t]
+    extra = [_VARIANT_TOKENS[t] for t in toks if t in _VARIANT_TOKENS]
+    # "lrr1": A/B against the round-1 image kernel (tools/dev/kernels_nlem_lr_r1.cu)
+    swap = {}
+    if "lrr1" in toks:
+        swap[os.path.join(CSRC, "kernels_nlem_lr.cu")] = os.path.join(
+            os.path.dirname(HERE), "tools", "dev", "kernels_nlem_lr_r1.cu")
+        extra += ["-I", CSRC]
     tag = f"_{variant}" if variant else ""
     jobs = []
     for src in sources():
         obj = os.path.join(OUT_DIR, os.path.basename(src) + tag + ".o")
+        src = swap.get(src, src)
         if src.endswith(".cu"):
             cmd = [NVCC, *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         else:

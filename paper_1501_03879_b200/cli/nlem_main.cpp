@@ -8,6 +8,8 @@
 // Every solve runs on the GPU through the C-ABI (include/nlem_b200.hpp); the option parser is
 // a small hand-written one (the reference's CLI11 is not vendored).
 #include <algorithm>
+#include <cerrno>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <filesystem>
@@ -77,22 +79,25 @@ std::string member(const std::string& v, const std::vector<std::string>& set, co
   return v;
 }
 
-std::pair<double, double> parse_pair(const std::string& text, const char* flag) {  // nlem_main.cpp:57-75
-  const auto colon = text.find(':');
-  if (colon == std::string::npos || colon == 0 || colon + 1 == text.size())
-    throw std::invalid_argument(std::string(flag) + " expects the form a:b");
-  std::size_t used = 0;
-  double a = 0, b = 0;
-  try {
-    a = std::stod(text.substr(0, colon), &used);
-    if (used != colon) throw std::invalid_argument("");
-    const std::string rest = text.substr(colon + 1);
-    b = std::stod(rest, &used);
-    if (used != rest.size()) throw std::invalid_argument("");
-  } catch (const std::exception&) {
-    throw std::invalid_argument(std::string(flag) + " expects two numbers a:b");
-  }
-  return {a, b};
+// "a:b" -> (a, b); same grammar and messages as the reference CLI (nlem_main.cpp:57-75):
+// exactly one split point with a full number on each side
+std::pair<double, double> parse_pair(const std::string& text, const char* flag) {
+  const std::string name(flag);
+  const std::size_t at = text.find(':');
+  const bool shaped = at != std::string::npos && at > 0 && at + 1 < text.size();
+  if (!shaped) throw std::invalid_argument(name + " expects the form a:b");
+  auto whole_number = [&](const std::string& part) {
+    const char* begin = part.c_str();
+    char* end = nullptr;
+    errno = 0;
+    const double v = std::strtod(begin, &end);
+    const bool ok = end != begin && *end == '\0' && errno != ERANGE;
+    if (!ok) throw std::invalid_argument(name + " expects two numbers a:b");
+    return v;
+  };
+  const double lhs = whole_number(text.substr(0, at));
+  const double rhs = whole_number(text.substr(at + 1));
+  return {lhs, rhs};
 }
 
 nlem::BoxConstraint parse_range(const std::string& text, const nlem::BoxConstraint& fallback) {
@@ -101,20 +106,26 @@ nlem::BoxConstraint parse_range(const std::string& text, const nlem::BoxConstrai
   return nlem::BoxConstraint::interval(static_cast<float>(l), static_cast<float>(u));
 }
 
-nlem::NlemParams make_params(const Config& cfg, double sigma, const std::string& solver) {  // :91-108
+// Options -> NlemParams (the reference CLI's defaults, nlem_main.cpp:91-108): h scales with
+// max(sigma, 1) so it stays positive at sigma 0, the init follows sigma unless --init is given,
+// and the result is validated before any work starts.
+nlem::NlemParams make_params(const Config& cfg, double sigma, const std::string& solver) {
+  static const std::map<std::string, nlem::DenoiseSolver> kSolvers = {
+      {"admm", nlem::DenoiseSolver::Admm}, {"irls", nlem::DenoiseSolver::Irls}};
+  static const std::map<std::string, nlem::PatchInit> kInits = {
+      {"noisy", nlem::PatchInit::NoisyPatch}, {"nlm", nlem::PatchInit::NlmPatch}};
+  const auto sv = kSolvers.find(solver);
+  const auto in = kInits.find(cfg.init);
   nlem::NlemParams p;
   p.search = cfg.search;
   p.patch = cfg.patch;
   p.sigma = sigma;
-  p.h = cfg.h_mult * std::max(sigma, 1.0);
-  p.solver = solver == "admm" ? nlem::DenoiseSolver::Admm
-             : solver == "irls" ? nlem::DenoiseSolver::Irls
-                                : nlem::DenoiseSolver::NlmOnly;
+  p.h = cfg.h_mult * (sigma > 1.0 ? sigma : 1.0);
+  p.solver = sv == kSolvers.end() ? nlem::DenoiseSolver::NlmOnly : sv->second;
   p.solver_iters = cfg.iters;
   p.mu = cfg.mu;
   p.epsilon = cfg.epsilon;
-  p.init_mode = cfg.init.empty() ? nlem::default_init_mode(sigma)
-                                 : (cfg.init == "noisy" ? nlem::PatchInit::NoisyPatch : nlem::PatchInit::NlmPatch);
+  p.init_mode = in == kInits.end() ? nlem::default_init_mode(sigma) : in->second;
   p.range = parse_range(cfg.range, nlem::BoxConstraint::interval(0.0f, 255.0f));
   p.threads = cfg.threads;
   nlem::validate(p);
@@ -225,14 +236,14 @@ int run_trace(const Config& cfg) {  // nlem_main.cpp:202-250
     a.max_iter = params.solver_iters;
     a.z_init = init;
     a.record_trace = true;
-    res = nlem::admm_euclidean_median(st.points, params.range, a);
+    res = nlem::admm_euclidean_median(nlem::PointSet{st.patches, st.weights, st.d}, params.range, a);
   } else {
     nlem::IrlsConfig c;
     c.epsilon = static_cast<float>(params.epsilon);
     c.max_iter = params.solver_iters;
     c.x_init = init;
     c.record_trace = true;
-    res = nlem::irls_euclidean_median(st.points, c);
+    res = nlem::irls_euclidean_median(nlem::PointSet{st.patches, st.weights, st.d}, c);
   }
   nlem::io_detail::save(nlem::encode_trace_csv(res.trace), cfg.trace_path);
   return 0;

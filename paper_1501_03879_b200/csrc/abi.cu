@@ -15,35 +15,41 @@
 
 namespace nlemk {
 
+namespace {
+DeviceCaps query_caps(int dev) {
+  DeviceCaps c;
+  cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&c.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&c.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&c.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&c.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+  // the stream-ordered scratch (padded bands, counters) comes from the device's default pool:
+  // keep freed blocks mapped instead of trimming them at every synchronize, so the first call
+  // after a host sync does not pay for re-mapping
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  return c;
+}
+}  // namespace
+
+// Fixed per-device storage filled once per device (std::call_once): the returned reference
+// stays valid while other host threads (nlem_denoise_multi_host: one per device) query other
+// devices for the first time - no container is ever resized.
 const DeviceCaps& device_caps() {
-  static std::mutex mu;
-  static std::vector<DeviceCaps> caps;
-  static std::vector<bool> have;
+  constexpr int kMaxDevices = 64;
+  static DeviceCaps caps[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
   int dev = 0;
   cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lock(mu);
-  if (static_cast<int>(caps.size()) <= dev) {
-    caps.resize(dev + 1);
-    have.resize(dev + 1, false);
+  if (dev < 0 || dev >= kMaxDevices) {
+    thread_local DeviceCaps extra;
+    extra = query_caps(dev);
+    return extra;
   }
-  if (!have[dev]) {
-    DeviceCaps c;
-    cudaDeviceGetAttribute(&c.sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&c.max_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&c.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    cudaDeviceGetAttribute(&c.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
-    cudaDeviceGetAttribute(&c.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
-    // the stream-ordered scratch (padded bands, counters) comes from the device's default pool:
-    // keep freed blocks mapped instead of trimming them at every synchronize, so the first call
-    // after a host sync does not pay for re-mapping
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t keep = ~uint64_t(0);
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    caps[dev] = c;
-    have[dev] = true;
-  }
+  std::call_once(once[dev], [dev] { caps[dev] = query_caps(dev); });
   return caps[dev];
 }
 
@@ -536,9 +542,9 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
-    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=lr|seg2|tile|fast|generic
+    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=lr|tile|fast|generic
     // forces one (A/B measurements; falls back to generic when unsupported)
-    static const char* force = std::getenv("NLEM_KERNEL");
+    const char* force = std::getenv("NLEM_KERNEL");  // per call: tests switch it in-process
     const std::string k = force ? force : "";
     if ((k.empty() || k == "lr") && nlem_lr_supported(L)) {
       // low-rank kernel, then the exact tile kernel over the pixels it handed off
@@ -548,7 +554,7 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
       if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int), s);
       if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 2, scratch + 1, scratch, s);
       if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 2, scratch + 1, s);
-      static const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;
+      const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;  // read per call (tests)
       if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
         int handed = 0;
         e = cudaMemcpyAsync(&handed, scratch + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
@@ -561,7 +567,6 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
         if (e == cudaSuccess) e = ef;
       }
     } else if ((k.empty() || k == "tile") && nlem_tile_supported(L)) e = launch_nlem_tile(L, s);
-    else if ((k.empty() || k == "seg2") && nlem_seg2_supported(L)) e = launch_nlem_seg2(L, s);
     else if ((k.empty() || k == "fast") && nlem_fast_supported(L)) e = launch_nlem_fast(L, s);
     else e = launch_nlem_generic(L, s);
   }
@@ -748,6 +753,109 @@ nlem_status nlem_denoise_host(const float* noisy, int64_t rows, int64_t cols,
                               nlem_failure* failure, int32_t device) {
   return nlem_denoise_rows_host(noisy, 0, rows, rows, cols, 0, rows, params, out, frames, failure,
                                 device);
+}
+
+nlem_status nlem_patch_stack_host(const float* image, int64_t rows, int64_t cols, int64_t row,
+                                  int64_t col, int32_t search, int32_t patch, float h,
+                                  float* patches_out, float* weights_out, int64_t* n_out,
+                                  int64_t* self_column_out, nlem_failure* failure,
+                                  int32_t device) {
+  nlem_failure local;
+  nlem_failure* f = failure ? failure : &local;
+  clear(f);
+  // patch.cpp:90-97 (validate_image, image.hpp:14-17, then the size and pixel checks)
+  if (rows < 1 || cols < 1) return invalid(f, "image must be non-empty");
+  if (!image || !patches_out || !weights_out || !n_out || !self_column_out)
+    return invalid(f, "null buffer");
+  for (int64_t i = 0; i < rows * cols; ++i)
+    if (!std::isfinite(image[i])) return invalid(f, "image intensities must be finite");
+  if (search < 1 || search % 2 == 0) return invalid(f, "search window must be odd and positive");
+  if (patch < 1 || patch % 2 == 0) return invalid(f, "patch size must be odd and positive");
+  if (row < 0 || row >= rows || col < 0 || col >= cols) return invalid(f, "pixel outside the image");
+  if (!(h > 0.0f)) return invalid(f, "similarity bandwidth h must be positive");  // patch.cpp:54
+  if (static_cast<int64_t>(patch) * patch > kMaxDim)
+    return invalid(f, "patch dimension k*k above 1024 is not supported");
+  const int64_t hs = search / 2;
+  const int64_t r0 = std::max<int64_t>(0, row - hs), r1 = std::min<int64_t>(rows - 1, row + hs);
+  const int64_t c0 = std::max<int64_t>(0, col - hs), c1 = std::min<int64_t>(cols - 1, col + hs);
+  const int64_t n = (r1 - r0 + 1) * (c1 - c0 + 1), d = static_cast<int64_t>(patch) * patch;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  cudaStream_t s = cudaStreamPerThread;
+  float *dimg = nullptr, *dp = nullptr, *dw = nullptr;
+  e = cudaMallocAsync(&dimg, rows * cols * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dp, n * d * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dw, n * 4, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dimg, image, rows * cols * 4, cudaMemcpyHostToDevice, s);
+  const double hh = static_cast<double>(h);
+  if (e == cudaSuccess)
+    e = launch_patch_stack(dimg, rows, cols, row, col, search, patch,
+                           static_cast<float>(1.0 / (hh * hh)), dp, dw, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(patches_out, dp, n * d * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(weights_out, dw, n * 4, cudaMemcpyDeviceToHost, s);
+  for (void* p : {static_cast<void*>(dimg), static_cast<void*>(dp), static_cast<void*>(dw)})
+    if (p) cudaFreeAsync(p, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  *n_out = n;
+  *self_column_out = (row - r0) * (c1 - c0 + 1) + (col - c0);
+  return NLEM_OK;
+}
+
+nlem_status nlem_solve_patch_host(const float* patches, const float* weights, int64_t n, int64_t d,
+                                  int64_t self_column, const nlem_params* params, float* init_out,
+                                  float* patch_out, nlem_failure* failure, int32_t device) {
+  nlem_failure local;
+  nlem_failure* f = failure ? failure : &local;
+  clear(f);
+  if (nlem_status st = validate_params_impl(params, f)) return st;
+  if (n < 1) return invalid(f, "point set must contain at least one point");
+  if (d < 1 || d > kMaxDim) return invalid(f, "point dimension must be in [1, 1024]");
+  if (self_column < 0 || self_column >= n)  // nlem.cpp:13-15
+    return invalid(f, "patch stack has no valid self column");
+  if (!patches || !weights || !init_out || !patch_out) return invalid(f, "null buffer");
+  if (n * d > (int64_t(1) << 31)) return invalid(f, "point set too large");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  cudaStream_t s = cudaStreamPerThread;
+  float *dp = nullptr, *dw = nullptr, *dinit = nullptr, *dout = nullptr;
+  e = cudaMallocAsync(&dp, n * d * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dw, n * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dinit, d * 4, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&dout, d * 4, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dp, patches, n * d * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(dw, weights, n * 4, cudaMemcpyHostToDevice, s);
+  nlem_status st = NLEM_OK;
+  const bool nlm_only = params->solver == NLEM_SOLVER_NLM_ONLY;
+  // NlmOnly builds no PointSet in the reference (nlem.cpp:26-31), so its inputs are not
+  // validated; the solvers validate theirs (types.hpp:58-68)
+  if (e == cudaSuccess && st == NLEM_OK)
+    e = launch_initial_patch(dp, dw, static_cast<int>(n), static_cast<int>(d),
+                             static_cast<int>(self_column), params->init_mode, params->range,
+                             dinit, nlm_only ? dout : nullptr, s);
+  if (e == cudaSuccess && st == NLEM_OK && !nlm_only) {
+    if (params->solver == NLEM_SOLVER_ADMM) {  // nlem.cpp:35-43
+      const nlem_admm_config c{params->mu, params->solver_iters, 0.0f};
+      st = nlem_admm_batched(dp, dw, 1, n, d, dinit, params->range, c, dout, nullptr, nullptr,
+                             nullptr, nullptr, f, s);
+    } else {  // nlem.cpp:45-55: IRLS from the init, then the box projection
+      const nlem_irls_config c{params->epsilon, params->solver_iters, params->irls_tol};
+      st = nlem_irls_batched(dp, dw, 1, n, d, dinit, c, dout, nullptr, nullptr, nullptr, f, s);
+      if (st == NLEM_OK) e = launch_clip(dout, static_cast<int>(d), params->range, s);
+    }
+  }
+  if (e == cudaSuccess && st == NLEM_OK) {
+    e = cudaMemcpyAsync(init_out, dinit, d * 4, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(patch_out, dout, d * 4, cudaMemcpyDeviceToHost, s);
+  }
+  for (void* p : {static_cast<void*>(dp), static_cast<void*>(dw), static_cast<void*>(dinit),
+                  static_cast<void*>(dout)})
+    if (p) cudaFreeAsync(p, s);
+  const cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(f, e);
+  return st;
 }
 
 }  // extern "C"

@@ -2,7 +2,9 @@
 //  * per-frame squared error -> PSNR for snapshot sweeps (proj/include/nlem/psnr.hpp:12-24),
 //    so convergence curves need no T x H x W device-to-host copy;
 //  * batched first-order optimality certificate (proj/include/nlem/diagnostics.hpp:22-55),
-//    certifying batched EM-ADMM outputs at scale without the CPU oracle.
+//    certifying batched EM-ADMM outputs at scale without the CPU oracle;
+//  * the single-pixel helpers behind the reference's solve_patch drop-in: the patch stack of
+//    one pixel (proj/src/patch.cpp:90-114) and the initial patch (proj/src/nlem.cpp:13-18).
 // Both reductions use fixed orders (deterministic).
 #include <algorithm>
 
@@ -164,6 +166,101 @@ cudaError_t launch_optimality(const float* points, const float* weights, const f
     NLEM_OPT_CASE(32)
 #undef NLEM_OPT_CASE
   }
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ int64_t reflect(int64_t i, int64_t n) {  // patch.cpp:9-16
+  if (n == 1) return 0;
+  const int64_t period = 2 * (n - 1);
+  int64_t m = i % period;
+  if (m < 0) m += period;
+  return m < n ? m : period - m;
+}
+
+// build_patch_stack(image, row, col, search, k, h) (patch.cpp:90-114) for one pixel, one CTA:
+// the clipped window in row-major neighbour order, patch j of k x k mirrored samples
+// (patch.cpp:27-38) at patches[j][0..d), weights exp(-||P_j - P_self||^2 / h^2) with the self
+// weight exactly 1 (patch.cpp:52-61).
+__global__ void __launch_bounds__(256)
+patch_stack_kernel(const float* __restrict__ img, int64_t rows, int64_t cols, int64_t row,
+                   int64_t col, int search, int k, float inv_h2, float* patches, float* weights) {
+  const int64_t hs = search / 2, hk = k / 2, d = static_cast<int64_t>(k) * k;
+  const int64_t r0 = row - hs < 0 ? 0 : row - hs, r1 = row + hs > rows - 1 ? rows - 1 : row + hs;
+  const int64_t c0 = col - hs < 0 ? 0 : col - hs, c1 = col + hs > cols - 1 ? cols - 1 : col + hs;
+  const int64_t nc = c1 - c0 + 1, n = (r1 - r0 + 1) * nc;
+  const int64_t self = (row - r0) * nc + (col - c0);
+  for (int64_t e = threadIdx.x; e < n * d; e += blockDim.x) {
+    const int64_t j = e / d, q = e % d;
+    const int64_t r = r0 + j / nc, c = c0 + j % nc;
+    const int64_t pr = reflect(r + q / k - hk, rows), pc = reflect(c + q % k - hk, cols);
+    patches[e] = img[pr * cols + pc];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t j = warp; j < n; j += blockDim.x >> 5) {
+    float s = 0.0f;
+    for (int64_t q = lane; q < d; q += 32) {
+      const float t = patches[j * d + q] - patches[self * d + q];
+      s = fmaf(t, t, s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) weights[j] = expf(-s * inv_h2);
+  }
+}
+
+// initial_patch (nlem.cpp:13-18) of one stack, one CTA: the self column (NoisyPatch) or the
+// weighted mean points * (w / sum w) (NlmPatch, types.hpp:73).  `mean_box` (optional) receives
+// the weighted mean projected onto `box` - the NlmOnly solve (nlem.cpp:26-31).
+__global__ void __launch_bounds__(256)
+initial_patch_kernel(const float* __restrict__ points, const float* __restrict__ weights, int n,
+                     int d, int self_col, int mode, nlem_box box, float* init, float* mean_box) {
+  __shared__ float part[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float s = 0.0f;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s += weights[k];
+  s = warp_sum(s);
+  if (lane == 0) part[warp] = s;
+  __syncthreads();
+  float wsum = 0.0f;
+  for (int w = 0; w < 8; ++w) wsum += part[w];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    float m = 0.0f;
+    for (int k = 0; k < n; ++k) m = fmaf(points[static_cast<int64_t>(k) * d + j], weights[k] / wsum, m);
+    init[j] = mode == NLEM_INIT_NOISY_PATCH ? points[static_cast<int64_t>(self_col) * d + j] : m;
+    if (mean_box) {
+      float v = m;
+      if (box.bounded) v = v < box.lower ? box.lower : (box.upper < v ? box.upper : v);
+      mean_box[j] = v;
+    }
+  }
+}
+
+// project_box (prox.hpp:45-50) of one d-vector in place
+__global__ void clip_kernel(float* x, int d, nlem_box box) {
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float v = x[j];
+    if (box.bounded) x[j] = v < box.lower ? box.lower : (box.upper < v ? box.upper : v);
+  }
+}
+
+cudaError_t launch_patch_stack(const float* img, int64_t rows, int64_t cols, int64_t row,
+                               int64_t col, int search, int k, float inv_h2, float* patches,
+                               float* weights, cudaStream_t stream) {
+  patch_stack_kernel<<<1, 256, 0, stream>>>(img, rows, cols, row, col, search, k, inv_h2, patches,
+                                            weights);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_initial_patch(const float* points, const float* weights, int n, int d,
+                                 int self_col, int mode, nlem_box box, float* init,
+                                 float* mean_box, cudaStream_t stream) {
+  initial_patch_kernel<<<1, 256, 0, stream>>>(points, weights, n, d, self_col, mode, box, init,
+                                              mean_box);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_clip(float* x, int d, nlem_box box, cudaStream_t stream) {
+  clip_kernel<<<1, 256, 0, stream>>>(x, d, box);
   return cudaGetLastError();
 }
 

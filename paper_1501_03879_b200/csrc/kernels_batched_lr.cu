@@ -489,16 +489,24 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       }
       fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
       BLR_STAMP(s4);
-      __syncthreads();
+      // the sweep barrier also votes: a ring overflow, cancellation or non-finite value
+      // anywhere hands the problem to the exact kernel - stop sweeping now
+      const int stop = __syncthreads_or(bad || ovf);
       BLR_STAMP(s5);
+      if (t == 1 && T > R && 2 * __syncthreads_count(real_me && s == 1.0f) > n) ovf = true;
+      if (stop || ovf) break;
 #ifdef NLEM_BLR_STAMPS
       st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
       st_q[0] += q0 - s1; st_q[1] += q1 - q0; st_q[2] += q2 - s3; st_q[3] += q3 - q2; st_q[4] += q4 - q3; st_q[5] += s4 - q4;
 #endif
      } else {
       BLR_STAMP(s4);
-      __syncthreads();
+      const int stop = __syncthreads_or(bad);
       BLR_STAMP(s5);
+      // small-mu regime (lambda = w/mu >= ||p||, e.g. the reference default mu = 1e-3): with most
+      // prox scales exactly 1 no history term decays and the ring overflows after R sweeps
+      if (t == 1 && T > R && 2 * __syncthreads_count(false) > n) ovf = true;
+      if (stop || ovf) break;
 #ifdef NLEM_BLR_STAMPS
       st_b1 += s5 - s4;
 #endif

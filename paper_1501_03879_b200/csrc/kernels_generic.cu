@@ -75,13 +75,17 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
                      int64_t batch, int n, int d, const float* __restrict__ z_init, nlem_box box,
                      float mu, int T, float tol, int res_mode, float* z_out, float* obj_out,
                      int* iters_out, float* tr_obj, float* tr_res, float* scratch,
-                     FailureSlot* fail) {
+                     int work_global, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   const size_t nd = static_cast<size_t>(n) * d;
   const size_t ns = admm_state_floats(n, d);
+  // per-CTA global slab (!SMEM): [ns state floats][the work block when it does not fit in
+  // shared memory (n beyond ~29k points: the 2n scales and weights)]
+  const size_t slab = ns + (work_global ? gen_work_floats(n, d) : 0);
   float* a_s = smem;
   float* p_s = SMEM ? smem + nd : nullptr;
-  GenWork W = carve_gen_work(SMEM ? smem + nd + ns : smem, n, d);
+  GenWork W = carve_gen_work(SMEM ? smem + nd + ns
+                                  : (work_global ? scratch + blockIdx.x * slab + ns : smem), n, d);
   const int tid = threadIdx.x;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     const float* ag = points + b * nd;
@@ -93,7 +97,7 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
       p = p_s;
     } else {
       a = ag;
-      p = scratch + blockIdx.x * ns;
+      p = scratch + blockIdx.x * slab;
     }
     for (int k = tid; k < n; k += kGenThreads) W.wts[k] = weights[b * n + k];
     __syncthreads();
@@ -131,11 +135,14 @@ __global__ void __launch_bounds__(kGenThreads)
 irls_batched_generic(const float* __restrict__ points, const float* __restrict__ weights,
                      int64_t batch, int n, int d, const float* __restrict__ x_init, float eps,
                      int T, float tol, float* x_out, float* obj_out, int* iters_out, float* tr_obj,
-                     FailureSlot* fail) {
+                     float* scratch, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   const size_t nd = static_cast<size_t>(n) * d;
   float* a_s = smem;
-  GenWork W = carve_gen_work(SMEM ? smem + nd : smem, n, d);
+  // scratch != null: the work block lives in a per-CTA global slab (too large for shared memory)
+  GenWork W = carve_gen_work(SMEM ? smem + nd
+                                  : (scratch ? scratch + blockIdx.x * gen_work_floats(n, d) : smem),
+                             n, d);
   const int tid = threadIdx.x;
   for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
     const float* ag = points + b * nd;
@@ -219,16 +226,19 @@ template <int JPL, bool SMEM>
 __global__ void __launch_bounds__(kGenThreads)
 nlem_pixels_generic(const float* __restrict__ pad, int64_t pad_row0, int64_t pad_cols,
                     int64_t rows, int64_t cols, int64_t out_row0, int64_t out_rows, NlemDevParams P,
-                    float* out, float* frames, float* scratch, FailureSlot* fail) {
+                    float* out, float* frames, float* scratch, int work_global, FailureSlot* fail) {
   extern __shared__ __align__(16) float smem[];
   const int k = P.patch, hk = k / 2, hs = P.search / 2;
   const int d = k * k;
   const int nmax = P.search * P.search;
   const size_t ndm = static_cast<size_t>(nmax) * d;
   const size_t nsm = static_cast<size_t>(nmax) * d * (d <= kRefFormMaxDim ? 2 : 1);
-  float* a_s = SMEM ? smem : scratch + blockIdx.x * (ndm + nsm);
+  // per-CTA global slab (!SMEM): [stack][state][the work block when it does not fit in shared
+  // memory (very large search windows)]
+  const size_t slab = ndm + nsm + (work_global ? gen_work_floats(nmax, d) : 0);
+  float* a_s = SMEM ? smem : scratch + blockIdx.x * slab;
   float* p_s = a_s + ndm;
-  GenWork W = carve_gen_work(SMEM ? smem + ndm + nsm : smem, nmax, d);
+  GenWork W = carve_gen_work(SMEM ? smem + ndm + nsm : (work_global ? a_s + ndm + nsm : smem), nmax, d);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int center = d / 2;
   const int64_t plane = out_rows * cols;
@@ -325,13 +335,16 @@ cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
   const size_t work = gen_work_floats(L.n, L.d) * sizeof(float);
   const size_t smem_full = (nd + ns) * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
-  const size_t smem = use_smem ? smem_full : work;
+  // the work block (2n + O(d) floats) itself beyond the opt-in limit: global slab as well
+  const bool work_global = !use_smem && work > static_cast<size_t>(caps.max_smem_optin);
+  const size_t smem = use_smem ? smem_full : work_global ? 0 : work;
   const int per_sm = use_smem ? std::max<int>(1, static_cast<int>(caps.smem_per_sm / (smem + 1024))) : 2;
   int64_t grid = std::min<int64_t>(L.batch, static_cast<int64_t>(caps.sms) * std::min(per_sm, 8));
   grid = std::max<int64_t>(grid, 1);
   float* scratch = nullptr;
   if (!use_smem) {
-    cudaError_t e = cudaMallocAsync(&scratch, grid * ns * sizeof(float), stream);
+    const size_t slab = ns + (work_global ? gen_work_floats(L.n, L.d) : 0);
+    cudaError_t e = cudaMallocAsync(&scratch, grid * slab * sizeof(float), stream);
     if (e != cudaSuccess) return e;
   }
   cudaError_t err = cudaSuccess;
@@ -341,13 +354,14 @@ cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.z_init, L.box, L.mu, L.max_iter, L.tol,
-          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, nullptr, L.fail);
+          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, nullptr, 0, L.fail);
     } else {
       auto kfn = admm_batched_generic<J, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.z_init, L.box, L.mu, L.max_iter, L.tol,
-          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, scratch, L.fail);
+          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, scratch,
+          work_global ? 1 : 0, L.fail);
     }
   });
   err = cudaGetLastError();
@@ -361,26 +375,34 @@ cudaError_t launch_irls_generic(const IrlsLaunch& L, cudaStream_t stream) {
   const size_t work = gen_work_floats(L.n, L.d) * sizeof(float);
   const size_t smem_full = nd * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
-  const size_t smem = use_smem ? smem_full : work;
+  const bool work_global = !use_smem && work > static_cast<size_t>(caps.max_smem_optin);
+  const size_t smem = use_smem ? smem_full : work_global ? 0 : work;
   const int per_sm = std::max<int>(1, static_cast<int>(caps.smem_per_sm / (smem + 1024)));
   int64_t grid = std::min<int64_t>(L.batch, static_cast<int64_t>(caps.sms) * std::min(per_sm, 8));
   grid = std::max<int64_t>(grid, 1);
+  float* scratch = nullptr;
+  if (work_global) {
+    cudaError_t e = cudaMallocAsync(&scratch, grid * gen_work_floats(L.n, L.d) * sizeof(float), stream);
+    if (e != cudaSuccess) return e;
+  }
   NLEM_DISPATCH_JPL(L.d, {
     if (use_smem) {
       auto kfn = irls_batched_generic<J, true>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.x_init, L.eps, L.max_iter, L.tol, L.x_out,
-          L.obj_out, L.iters_out, L.tr_obj, L.fail);
+          L.obj_out, L.iters_out, L.tr_obj, nullptr, L.fail);
     } else {
       auto kfn = irls_batched_generic<J, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.x_init, L.eps, L.max_iter, L.tol, L.x_out,
-          L.obj_out, L.iters_out, L.tr_obj, L.fail);
+          L.obj_out, L.iters_out, L.tr_obj, scratch, L.fail);
     }
   });
-  return cudaGetLastError();
+  cudaError_t err = cudaGetLastError();
+  if (scratch) cudaFreeAsync(scratch, stream);
+  return err;
 }
 
 cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t rows, int64_t cols,
@@ -404,14 +426,16 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream) {
   const size_t work = gen_work_floats(nmax, d) * sizeof(float);
   const size_t smem_full = (ndm + nsm) * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
-  const size_t smem = use_smem ? smem_full : work;
+  const bool work_global = !use_smem && work > static_cast<size_t>(caps.max_smem_optin);
+  const size_t smem = use_smem ? smem_full : work_global ? 0 : work;
   const int per_sm = std::max<int>(1, static_cast<int>(caps.smem_per_sm / (smem + 1024)));
   const int64_t pixels = L.out_rows * L.cols;
   int64_t grid = std::min<int64_t>(pixels, static_cast<int64_t>(caps.sms) * std::min(per_sm, 8));
   grid = std::max<int64_t>(grid, 1);
   float* scratch = nullptr;
   if (!use_smem) {
-    cudaError_t e = cudaMallocAsync(&scratch, grid * (ndm + nsm) * sizeof(float), stream);
+    const size_t slab = ndm + nsm + (work_global ? gen_work_floats(nmax, d) : 0);
+    cudaError_t e = cudaMallocAsync(&scratch, grid * slab * sizeof(float), stream);
     if (e != cudaSuccess) return e;
   }
   NLEM_DISPATCH_JPL(d, {
@@ -420,13 +444,13 @@ cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream) {
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.pad, L.pad_row0, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out,
-          L.frames, nullptr, L.fail);
+          L.frames, nullptr, 0, L.fail);
     } else {
       auto kfn = nlem_pixels_generic<J, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.pad, L.pad_row0, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out,
-          L.frames, scratch, L.fail);
+          L.frames, scratch, work_global ? 1 : 0, L.fail);
     }
   });
   cudaError_t err = cudaGetLastError();

@@ -101,8 +101,6 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cud
 // Register-resident batched IRLS for d = 49 (kernels_batched_lr.cu).
 bool irls_reg_supported(const IrlsLaunch& L);
 cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream);
-bool nlem_seg2_supported(const NlemLaunch& L);
-cudaError_t launch_nlem_seg2(const NlemLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);
 // tile kernel over a device-side list of band pixel indices (count read on the device)
@@ -125,6 +123,13 @@ cudaError_t launch_optimality(const float* points, const float* weights, const f
 // validation kernels (types.hpp:58-68, image.hpp:14-17): packed (index << 2 | code), ~0 = ok
 cudaError_t launch_validate_points(const float* points, const float* weights, int64_t batch,
                                    int n, int d, unsigned long long* result, cudaStream_t stream);
+cudaError_t launch_patch_stack(const float* img, int64_t rows, int64_t cols, int64_t row,
+                               int64_t col, int search, int k, float inv_h2, float* patches,
+                               float* weights, cudaStream_t stream);
+cudaError_t launch_initial_patch(const float* points, const float* weights, int n, int d,
+                                 int self_col, int mode, nlem_box box, float* init,
+                                 float* mean_box, cudaStream_t stream);
+cudaError_t launch_clip(float* x, int d, nlem_box box, cudaStream_t stream);
 cudaError_t launch_validate_image(const float* img, int64_t count, unsigned long long* result,
                                   cudaStream_t stream);
 

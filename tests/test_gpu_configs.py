@@ -1,0 +1,104 @@
+"""GPU parity at the BASELINE.json configurations as specified (not crops): the benchmarked
+config 3 (4096^2, sigma 30, k=7, S=21, T=10) on full-width rows at both image edges and in
+the interior, and config 4 (512^2, sigma 10/20/40/60, ADMM and IRLS T=1..100) on
+stride-sampled rows with PSNR per iteration.  The oracle is the FP64 restatement of
+proj/src/nlem.cpp:68-128 on the same float32 inputs.  Bar (north_star): max |GPU - oracle|
+<= 1e-2 gray levels and |dPSNR| <= 0.01 dB."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-2
+PSNR_TOL = 0.01
+
+
+def _psnr(a, clean):
+    return 10 * math.log10(255 ** 2 / float(np.mean((a.astype(np.float64) - clean) ** 2)))
+
+
+@pytest.fixture(scope="module")
+def nb():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1501_03879_b200 as nb
+
+    return nb
+
+
+@pytest.fixture(scope="module")
+def config3(nb):
+    """The whole benchmarked image through the production dispatch (low-rank kernel + exact
+    hand-off), once for the module."""
+    import torch
+
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(3)
+    p = nb.NlemParams(search=21, patch=7, h=synth.reference_h(30.0, 49), sigma=30.0, solver="admm",
+                      solver_iters=10, mu=1.0, init_mode="nlm")
+    out = nb.nlem_denoise(torch.from_numpy(noisy).cuda(), p).cpu().numpy()
+    return clean, noisy, out
+
+
+def test_config3_rows_vs_oracle(nb, oracle, config3):
+    """Rows 0-3 (clipped windows, mirrored patches at the top), three interior rows and rows
+    4092-4095 (bottom), full width (4096 pixels each, both side edges included)."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy, out = config3
+    o = oracle.make_params(search=21, patch=7, h=synth.reference_h(30.0, 49), sigma=30.0,
+                           solver="admm", solver_iters=10, mu=1.0, init_mode="nlm")
+    X = noisy.astype(np.float64)
+    rows = [0, 1, 2, 3, 1337, 2048, 3071, 4092, 4093, 4094, 4095]
+    ref = {}
+    for r0, r1 in ((0, 4), (1337, 1338), (2048, 2049), (3071, 3072), (4092, 4096)):
+        full = oracle.nlem_denoise(X, o, rows=(r0, r1))
+        for r in range(r0, r1):
+            ref[r] = full[r]
+    g = out[rows].astype(np.float64)
+    f = np.stack([ref[r] for r in rows])
+    err = np.abs(g - f)
+    assert err.max() <= TOL, (err.max(), np.unravel_index(err.argmax(), err.shape))
+    c = clean[rows].astype(np.float64)
+    assert abs(_psnr(g, c) - _psnr(f, c)) <= PSNR_TOL
+
+
+def test_config3_whole_image_sanity(config3):
+    """Every pixel finite and inside the box; denoising raises PSNR over the noisy input."""
+    clean, noisy, out = config3
+    assert np.isfinite(out).all() and out.min() >= 0.0 and out.max() <= 255.0
+    c = clean.astype(np.float64)
+    assert _psnr(out, c) > _psnr(noisy, c) + 5.0
+
+
+@pytest.mark.parametrize("sigma", [10.0, 20.0, 40.0, 60.0])
+def test_config4_sweep_vs_oracle(nb, oracle, sigma):
+    """Config 4: 512^2 (config-2 generator) at sigma, ADMM (mu=1, NLM init) and IRLS (eps=1e-4,
+    tol<0: a fixed count) emitting all 100 frames in one run as
+    nlem_denoise_snapshots does; every frame of 10 sampled rows (0, 511 and stride 57) matches
+    the oracle and the PSNR of the sample against the clean image agrees per iteration."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(2, sigma=sigma)
+    h = synth.reference_h(sigma, 49)
+    rows = sorted({0, 511} | set(range(29, 512, 57)))
+    X = noisy.astype(np.float64)
+    c = clean[rows].astype(np.float64)
+    for solver, kw in (("admm", dict(mu=1.0)), ("irls", dict(epsilon=1e-4, irls_tol=-1.0))):
+        g = nb.NlemParams(search=21, patch=7, h=h, sigma=sigma, solver=solver, solver_iters=100,
+                          init_mode="nlm", **kw)
+        fg = nb.nlem_denoise_snapshots(noisy, g)[:, rows, :].astype(np.float64)
+        o = oracle.make_params(search=21, patch=7, h=h, sigma=sigma, solver=solver, solver_iters=100,
+                               init_mode="nlm", **kw)
+        fo = np.empty_like(fg)
+        for i, r in enumerate(rows):
+            _, fr = oracle.nlem_denoise(X, o, rows=(r, r + 1), snapshots=True)
+            fo[:, i, :] = fr[:, r, :]
+        err = np.abs(fg - fo)
+        assert err.max() <= TOL, (solver, err.max(), np.unravel_index(err.argmax(), err.shape))
+        for t in range(100):
+            assert abs(_psnr(fg[t], c) - _psnr(fo[t], c)) <= PSNR_TOL, (solver, t)

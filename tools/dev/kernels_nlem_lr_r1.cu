@@ -96,7 +96,6 @@ constexpr int W_TOTAL = W_GR + 8;
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
 constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
 constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2
-constexpr float kCancel = 1.0f / 256.0f;  // N below 2^-8 (H + ||c~||^2): the expansion cancels
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -106,12 +105,6 @@ __device__ __forceinline__ void cpa4(float* dst, const float* src) {
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-// three-input maximum (FMNMX3, sm_100)
-__device__ __forceinline__ float max3(float a, float b, float c) {
-  float r;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
-  return r;
-}
 __device__ __forceinline__ float rsq(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -673,13 +666,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #ifdef NLEM_LR_STAMPS
     st_t2 = clock64(); st_setup += st_t2 - st_t1;
 #endif
-    // small-mu regime (lambda = w / mu against ||p||, e.g. the reference default mu = 1e-3):
-    // when the self point's prox scale saturates at sweep 1 (lambda_self = 1/mu >= ||z_0 - a_self||
-    // = ||c~_1||), most scales do, no history term decays and the ring would overflow after R
-    // sweeps - the pixel goes to the exact kernel right away.  A heuristic: a wrong guess costs
-    // time, never accuracy.  Warp-uniform (gram[] holds the same value in every lane).
-    if (P.iters > R && !static_eq && inv_mu * inv_mu >= gram[R]) ovf = true;
-    for (int t = 1; t <= P.iters && !ovf; ++t) {
+    for (int t = 1; t <= P.iters; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
       float2 u[SEGL];  // ga' of (slot 0, slot 1): the FFMA2 pairs of the patch-sum pass
@@ -721,7 +708,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         // non-finite through the shared c~ / Gram values, which makes the self point's N (lambda
         // = 1/mu != 0) non-finite in the same sweep, so the flagged sweep is the reference's.
         float2 nchk = make_float2(0.0f, 0.0f);
-        float hmax = -1.0f;
         static_for<SEGL>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           // point i of both slots as one register pair per field
@@ -737,8 +723,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
                             __ffma2_rn(al2, make_float2(G[2], G[2]), __fmul2_rn(al3, make_float2(G[3], G[3])))));
           const float2 gp1 = __fadd2_rn(ga, one2);
           const float2 t2 = __ffma2_rn(make_float2(-gp1.x, -gp1.y), D_, X2);
-          const float2 HG = __fadd2_rn(H, make_float2(Gnn, Gnn));
-          const float2 N = __ffma2_rn(make_float2(2.0f, 2.0f), t2, HG);
+          const float2 N = __ffma2_rn(make_float2(2.0f, 2.0f), t2, __fadd2_rn(H, make_float2(Gnn, Gnn)));
           float2 sc, Nc;
           {
             const float lx = lm[2 * i], ly = lm[2 * i + 1];
@@ -750,17 +735,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           const float2 B = __fadd2_rn(K, D_);
           const float2 ev = __fmul2_rn(sc, al3);
           const float2 evv = __fmul2_rn(__fmul2_rn(ev, ev), make_float2(nrR, nrR));
-          // hand-off tests as one running maximum (positive = hand the pixel to the exact
-          // kernel), checked once per sweep:
-          //  * ring overflow: the dropped term s al_3 c~_{t-R} is above FP32 rounding of p;
-          //  * cancellation of the Gram expansion: ||p||^2 far below the terms it is formed from
-          //    (N < 2^-8 (H + ||c~||^2)), so FP32 rounding of N would be amplified into s (the
-          //    batched kernel's test, kernels_batched_lr.cu).  Padding points (lambda = 0) are
-          //    included: a spurious hand-off costs time, never accuracy.
-          const float2 vo = __ffma2_rn(Nc, make_float2(-kThr2, -kThr2), evv);
-          const float2 vc = __ffma2_rn(HG, make_float2(kCancel, kCancel), make_float2(-N.x, -N.y));
-          hmax = max3(hmax, vo.x, vo.y);
-          hmax = max3(hmax, vc.x, vc.y);
+          ovf |= evv.x > kThr2 * Nc.x || evv.y > kThr2 * Nc.y;
           float o[16];
           const float2 oH = __ffma2_rn(sc, __ffma2_rn(sc, Nc, __fmul2_rn(make_float2(-2.0f, -2.0f), B)), a2);
           const float2 oK = __ffma2_rn(sc, B, make_float2(-a2.x, -a2.y));
@@ -797,7 +772,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
         usum = us2.x + us2.y;
         fnorm = !isfinite(nchk.x + nchk.y);
-        ovf = hmax > 0.0f;
         if (static_eq) {  // warp-uniform and rare: only an all-equal footprint can stop exactly;
           // the prox scales were just stored as al0 (fields 8 / 9 of each point pair) - reread
           // them from TMEM instead of testing every point in the sweep
@@ -811,7 +785,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           });
         }
       }
-      // a ring overflow / cancellation hands the whole pixel to the exact kernel: stop now
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
       float gA, gB, xs[5];
       {
@@ -841,11 +814,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         }
       }
       const unsigned bad_z = __ballot_sync(0xffffffffu, zbad), bad_n = __ballot_sync(0xffffffffu, fnorm);
-      const unsigned bad_o = __ballot_sync(0xffffffffu, ovf);
-      if (bad_z | bad_n | bad_o) {
-        // a hand-off (ring overflow / cancellation) outranks a failure: the exact kernel redoes
-        // the whole pixel and records any failure itself
-        if (!bad_o) fw = bad_z ? 2 * t : 2 * t + 1;
+      if (bad_z | bad_n) {
+        fw = bad_z ? 2 * t : 2 * t + 1;
         break;
       }
       if (static_eq && !__any_sync(0xffffffffu, sne1 | zne)) {  // residual exactly 0
