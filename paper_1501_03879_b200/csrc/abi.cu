@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "launch.h"
+#include "solver_generic.cuh"
 
 namespace nlemk {
 
@@ -415,11 +416,11 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
   L.fail = reinterpret_cast<FailureSlot*>(slot.ptr);
   if (lr) {
     // low-rank kernel, then the exact p-form kernel over the problems it handed off
-    int* scratch = nullptr;  // [0] hand-off count, [1..] hand-off list
-    e = cudaMallocAsync(&scratch, (1 + batch) * sizeof(int), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, sizeof(int), s);
-    if (e == cudaSuccess) e = launch_admm_lr(L, scratch + 1, scratch, s);
-    if (e == cudaSuccess) e = launch_admm_fast_list(L, scratch + 1, scratch, s);
+    int* scratch = nullptr;  // [0] hand-off count, [1] small-mu probe, [2..] hand-off list
+    e = cudaMallocAsync(&scratch, (2 + batch) * sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int), s);
+    if (e == cudaSuccess) e = launch_admm_lr(L, scratch + 2, scratch, scratch + 1, s);
+    if (e == cudaSuccess) e = launch_admm_fast_list(L, scratch + 2, scratch, s);
     const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;  // read per call (tests)
     if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
       int handed = 0;
@@ -434,6 +435,23 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
     }
   } else {
     e = admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
+  }
+  // Collinear point sets (affine rank 1) are one-dimensional problems: with tol 0 their exact
+  // residual stop is reachable (as for d <= 16) and only the reference-form sweep reproduces
+  // the reference's iteration count.  The p-form kernels above cannot tell, so such problems
+  // are re-solved in reference form.  Only the iteration count / trace length can differ (the
+  // iterate is at a fixed point after an exact stop), so this runs when they are requested.
+  if (e == cudaSuccess && L.res_mode == RES_EXACT0 && !use_ref_form(L.n, L.d) &&
+      (iters_out != nullptr || trace_objective != nullptr)) {
+    int* cl = nullptr;  // [0] count, [1..] problem list
+    e = cudaMallocAsync(&cl, (1 + batch) * sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(cl, 0, sizeof(int), s);
+    if (e == cudaSuccess) e = launch_collinear(points, batch, L.n, L.d, cl + 1, cl, s);
+    if (e == cudaSuccess) e = launch_admm_generic(L, s, cl + 1, cl, true);
+    if (cl) {
+      const cudaError_t ef = cudaFreeAsync(cl, s);
+      if (e == cudaSuccess) e = ef;
+    }
   }
   if (e != cudaSuccess) return cuda_fail(failure, e);
   if (!failure) return NLEM_OK;
@@ -548,19 +566,22 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     const std::string k = force ? force : "";
     if ((k.empty() || k == "lr") && nlem_lr_supported(L)) {
       // low-rank kernel, then the exact tile kernel over the pixels it handed off
-      int* scratch = nullptr;  // [0] work counter, [1] hand-off count, [2..] hand-off list
+      // [0] work counter, [1] hand-off count (-1: all), [2, 3] small-mu probe, [4..] hand-off list
+      int* scratch = nullptr;
       const int64_t pixels = out_rows * cols;
-      e = cudaMallocAsync(&scratch, (2 + pixels) * sizeof(int), s);
-      if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 2 * sizeof(int), s);
-      if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 2, scratch + 1, scratch, s);
-      if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 2, scratch + 1, s);
+      e = cudaMallocAsync(&scratch, (4 + pixels) * sizeof(int), s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 4 * sizeof(int), s);
+      int* probe = nlem_lr_probe_wanted(L) ? scratch + 2 : nullptr;
+      if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 4, scratch + 1, scratch, probe, s);
+      if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 4, scratch + 1, s);
       const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;  // read per call (tests)
       if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
         int handed = 0;
         e = cudaMemcpyAsync(&handed, scratch + 1, sizeof(int), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-        std::fprintf(stderr, "nlem_lr: %lld pixels, %d handed to the tile kernel\n",
-                     static_cast<long long>(pixels), handed);
+        std::fprintf(stderr, "nlem_lr: %lld pixels, %lld handed to the tile kernel\n",
+                     static_cast<long long>(pixels),
+                     handed < 0 ? static_cast<long long>(pixels) : static_cast<long long>(handed));
       }
       if (scratch) {
         const cudaError_t ef = cudaFreeAsync(scratch, s);

@@ -243,6 +243,85 @@ __global__ void clip_kernel(float* x, int d, nlem_box box) {
   }
 }
 
+// Collinear point sets: a_k = a_0 + t_k e for every k, not all equal (affine rank 1).  Such a
+// problem is one-dimensional along e, where the reference's exact-zero residual stop
+// (admm.hpp:77 with tol 0) is reachable as in d <= 16 (the reference-form range of the generic
+// kernel), so its iteration count is only reproduced by the reference-form sweep.  One CTA per
+// problem: e = a_k1 - a_0 for the lowest k1 with a_k1 != a_0, then every u_k = a_k - a_0 must
+// satisfy <u_k, e>^2 >= (1 - 1e-9) ||u_k||^2 ||e||^2 (FP64: exact for exactly collinear
+// float data).  The second pass re-reads the problem from L1 / L2.
+__global__ void __launch_bounds__(256)
+collinear_kernel(const float* __restrict__ points, int64_t batch, int n, int d, int* list,
+                 int* count) {
+  __shared__ int k1;
+  __shared__ int all_ok;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t nd = static_cast<int64_t>(n) * d;
+  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+    const float* a = points + b * nd;
+    if (threadIdx.x == 0) {
+      k1 = n;
+      all_ok = 1;
+    }
+    __syncthreads();
+    // pass 1: lowest point differing from a_0 (each thread stops at its first hit: its later
+    // elements belong to later points)
+    int mine = n;
+    for (int64_t e = d + threadIdx.x; e < nd; e += blockDim.x)
+      if (a[e] != a[e % d]) {
+        mine = static_cast<int>(e / d);
+        break;
+      }
+    mine = __reduce_min_sync(0xffffffffu, mine);
+    if (lane == 0 && mine < n) atomicMin(&k1, mine);
+    __syncthreads();
+    const int kk = k1;
+    if (kk < n) {
+      const float* ae = a + static_cast<int64_t>(kk) * d;
+      double ee = 0.0;
+      for (int j = lane; j < d; j += 32) {
+        const double u = static_cast<double>(ae[j]) - a[j];
+        ee = fma(u, u, ee);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ee += __shfl_xor_sync(0xffffffffu, ee, o);
+      // pass 2: every point parallel to e; a warp leaves as soon as any point is not (generic
+      // problems fail on their first points)
+      for (int k = kk + 1 + warp; k < n; k += 8) {
+        if (!*static_cast<volatile int*>(&all_ok)) break;
+        const float* ak = a + static_cast<int64_t>(k) * d;
+        double ue = 0.0, uu = 0.0;
+        for (int j = lane; j < d; j += 32) {
+          const double u = static_cast<double>(ak[j]) - a[j];
+          const double v = static_cast<double>(ae[j]) - a[j];
+          ue = fma(u, v, ue);
+          uu = fma(u, u, uu);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          ue += __shfl_xor_sync(0xffffffffu, ue, o);
+          uu += __shfl_xor_sync(0xffffffffu, uu, o);
+        }
+        if (!(ue * ue >= (1.0 - 1e-9) * uu * ee)) {
+          if (lane == 0) all_ok = 0;  // benign race: every writer stores 0
+          break;
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0 && all_ok) list[atomicAdd(count, 1)] = static_cast<int>(b);
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_collinear(const float* points, int64_t batch, int n, int d, int* list,
+                             int* count, cudaStream_t stream) {
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(batch, device_caps().sms * 8));
+  collinear_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(points, batch, n, d, list,
+                                                                     count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_patch_stack(const float* img, int64_t rows, int64_t cols, int64_t row,
                                int64_t col, int search, int k, float inv_h2, float* patches,
                                float* weights, cudaStream_t stream) {

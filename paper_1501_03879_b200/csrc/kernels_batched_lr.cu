@@ -58,6 +58,7 @@ constexpr int R = 4;
 constexpr int RS = 64;
 constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2: ring term below FP32 rounding
 constexpr float kCancel = 1.0f / 256.0f;           // N below 2^-8 (H + ||c~||^2): cancellation
+constexpr int kProbe = 64;                         // problems sampled by the small-mu probe
 // shared memory (floats)
 constexpr int SM_STAGE = 0;                      // raw points of the next problem (+4 shift)
 constexpr int SM_WST = SM_STAGE + NCAP * D + 4;  // raw weights of the next problem (+4 shift)
@@ -269,7 +270,20 @@ __global__ void __launch_bounds__(ALL, 1)
 admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
                 int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                 int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
-                int* ho_count, unsigned long long* invalid) {
+                int* ho_count, unsigned long long* invalid, int probe_n, int* probe_count) {
+  // probe_n > 0 (probe launch): probe_n problems spread evenly over the batch run up to the
+  // small-mu decision of sweep 1 and count predicted hand-offs into *probe_count; no outputs.
+  // probe_n == 0 with probe_count (main launch): when more than 90 % of the probed problems
+  // would be handed off (the small-mu regime), every problem is, right after its fused input
+  // validation - the exact p-form kernel then takes the whole batch (deterministic: the
+  // decision depends on the input only).
+  bool all_mode = false;
+  if (probe_n == 0 && probe_count != nullptr) {
+    const int64_t pt = batch < kProbe ? batch : kProbe;
+    all_mode = 10 * static_cast<int64_t>(*static_cast<volatile int*>(probe_count)) > 9 * pt;
+  }
+  const int64_t nidx = probe_n ? probe_n : batch;
+  auto prob_of = [&](int64_t i) { return probe_n ? i * batch / probe_n : i; };
   extern __shared__ __align__(16) float smem[];
   float* const stage = smem + SM_STAGE;
   float* const wst = smem + SM_WST;
@@ -301,14 +315,15 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #ifdef NLEM_BLR_STAMPS
   long long su_wait = 0, su_load = 0, su_pref = 0, su_init = 0, su_sw = 0, su_epi = 0, su_n = 0;
 #endif
-  int64_t b = blockIdx.x;
-  if (b < batch) {
+  int64_t b = prob_of(blockIdx.x);
+  if (static_cast<int64_t>(blockIdx.x) < nidx) {
     stage_copy(stage, points + b * nd, nd);
     stage_copy(wst, weights + b * n, n);
   }
   cp_commit();
 
-  for (; b < batch; b += gridDim.x) {
+  for (int64_t ib = blockIdx.x; ib < nidx; ib += gridDim.x) {
+    b = prob_of(ib);
 #ifdef NLEM_BLR_STAMPS
     const long long su_t0 = clock64();
 #endif
@@ -348,14 +363,19 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #ifdef NLEM_BLR_STAMPS
     const long long su_t2 = clock64(); su_load += su_t2 - su_t1;
 #endif
-    const int64_t bn = b + gridDim.x;
-    if (bn < batch) {
+    if (ib + gridDim.x < nidx) {
+      const int64_t bn = prob_of(ib + gridDim.x);
       stage_copy(stage, points + bn * nd, nd);
       stage_copy(wst, weights + bn * n, n);
     }
     cp_commit();
-    if (static_eq) {  // exact stop possible: the p-form kernel decides it structurally
-      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+    // exact stop possible (the p-form kernel decides it structurally), or the whole batch
+    // goes to the exact kernel (all_mode)
+    if (static_eq || all_mode) {
+      if (tid == 0) {
+        if (probe_n) atomicAdd(probe_count, 1);
+        else ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      }
       continue;
     }
 
@@ -494,7 +514,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       const int stop = __syncthreads_or(bad || ovf);
       BLR_STAMP(s5);
       if (t == 1 && T > R && 2 * __syncthreads_count(real_me && s == 1.0f) > n) ovf = true;
-      if (stop || ovf) break;
+      if (stop || ovf || probe_n) break;
 #ifdef NLEM_BLR_STAMPS
       st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
       st_q[0] += q0 - s1; st_q[1] += q1 - q0; st_q[2] += q2 - s3; st_q[3] += q3 - q2; st_q[4] += q4 - q3; st_q[5] += s4 - q4;
@@ -506,7 +526,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       // small-mu regime (lambda = w/mu >= ||p||, e.g. the reference default mu = 1e-3): with most
       // prox scales exactly 1 no history term decays and the ring overflows after R sweeps
       if (t == 1 && T > R && 2 * __syncthreads_count(false) > n) ovf = true;
-      if (stop || ovf) break;
+      if (stop || ovf || probe_n) break;
 #ifdef NLEM_BLR_STAMPS
       st_b1 += s5 - s4;
 #endif
@@ -578,9 +598,13 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
-      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      if (tid == 0) {
+        if (probe_n) atomicAdd(probe_count, 1);
+        else ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
+      }
       continue;
     }
+    if (probe_n) continue;
     if (warp == CW) {
       if (cv0) z_out[b * D + cj] = z0;
       if (cv1) z_out[b * D + cj + 1] = z1;
@@ -854,15 +878,26 @@ bool admm_lr_supported(const AdmmLaunch& L) {
          static_cast<int64_t>(L.n) * D < (int64_t(1) << 31) / 4;
 }
 
-cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cudaStream_t stream) {
+cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int* probe,
+                           cudaStream_t stream) {
   auto kfn = admm_batched_lr;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
+  const int sms = device_caps().sms;
+  if (probe != nullptr && L.max_iter > R) {  // small-mu probe (probe[0] = predicted hand-offs)
+    const int pn = static_cast<int>(std::min<int64_t>(L.batch, kProbe));
+    kfn<<<static_cast<unsigned>(std::min(pn, sms)), ALL, SMEM_BYTES, stream>>>(
+        L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
+        L.iters_out, ho_list, ho_count, L.invalid, pn, probe);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  } else {
+    probe = nullptr;
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
-      L.iters_out, ho_list, ho_count, L.invalid);
+      L.iters_out, ho_list, ho_count, L.invalid, 0, probe);
   return cudaGetLastError();
 }
 

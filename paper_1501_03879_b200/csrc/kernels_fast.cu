@@ -426,7 +426,7 @@ nlem_pixels_fast(const float* __restrict__ pad, int64_t pad_row0, int64_t pad_co
   S.carve(smem);
   float* tile = smem + FastSmem<C>::TOTAL;
   __shared__ int next_chunk;
-  const int k = P.patch, hk = k / 2, SW = P.search, hs = SW / 2;
+  const int k = P.patch, SW = P.search, hs = SW / 2;
   const int TW = SW + k - 1;  // tile side
   const int center = C::D / 2;
   const int self = hs * SW + hs;

@@ -75,10 +75,14 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
                      int64_t batch, int n, int d, const float* __restrict__ z_init, nlem_box box,
                      float mu, int T, float tol, int res_mode, float* z_out, float* obj_out,
                      int* iters_out, float* tr_obj, float* tr_res, float* scratch,
-                     int work_global, FailureSlot* fail) {
+                     int work_global, FailureSlot* fail, const int* list, const int* list_count,
+                     int force_ref) {
+  // list: only the listed problems (in list order); force_ref: the reference-form sweep for
+  // every problem (collinear point sets, see collinear_kernel)
   extern __shared__ __align__(16) float smem[];
   const size_t nd = static_cast<size_t>(n) * d;
-  const size_t ns = admm_state_floats(n, d);
+  const size_t ns = admm_state_floats(n, d, force_ref != 0);
+  const int64_t count = list ? static_cast<int64_t>(*list_count) : batch;
   // per-CTA global slab (!SMEM): [ns state floats][the work block when it does not fit in
   // shared memory (n beyond ~29k points: the 2n scales and weights)]
   const size_t slab = ns + (work_global ? gen_work_floats(n, d) : 0);
@@ -87,7 +91,8 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
   GenWork W = carve_gen_work(SMEM ? smem + nd + ns
                                   : (work_global ? scratch + blockIdx.x * slab + ns : smem), n, d);
   const int tid = threadIdx.x;
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
+  for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
+    const int64_t b = list ? static_cast<int64_t>(list[i]) : i;
     const float* ag = points + b * nd;
     const float* a;
     float* p;
@@ -110,7 +115,7 @@ admm_batched_generic(const float* __restrict__ points, const float* __restrict__
     const SolveStatus st =
         admm_solve_generic<JPL>(a, W.wts, p, n, d, W, box, mu, T, tol, res_mode,
                                 tr_obj ? tr_obj + b * T : nullptr, tr_res ? tr_res + b * T : nullptr,
-                                NoSnapshot{});
+                                NoSnapshot{}, force_ref != 0);
     __syncthreads();
     if (st.fail_iter >= 0) {
       if (tid == 0) record_failure(fail, b, st.fail_iter, st.fail_kind);
@@ -328,10 +333,11 @@ int jpl_for(int d) {
     default: { constexpr int J = 32; __VA_ARGS__; break; } \
   }
 
-cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
+cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream, const int* list,
+                                const int* list_count, bool force_ref) {
   const DeviceCaps& caps = device_caps();
   const size_t nd = static_cast<size_t>(L.n) * L.d;
-  const size_t ns = admm_state_floats(L.n, L.d);
+  const size_t ns = admm_state_floats(L.n, L.d, force_ref);
   const size_t work = gen_work_floats(L.n, L.d) * sizeof(float);
   const size_t smem_full = (nd + ns) * sizeof(float) + work;
   const bool use_smem = smem_full <= static_cast<size_t>(caps.max_smem_optin);
@@ -354,14 +360,15 @@ cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream) {
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.z_init, L.box, L.mu, L.max_iter, L.tol,
-          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, nullptr, 0, L.fail);
+          L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, nullptr, 0, L.fail,
+          list, list_count, force_ref ? 1 : 0);
     } else {
       auto kfn = admm_batched_generic<J, false>;
       cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
       kfn<<<static_cast<unsigned>(grid), kGenThreads, smem, stream>>>(
           L.points, L.weights, L.batch, L.n, L.d, L.z_init, L.box, L.mu, L.max_iter, L.tol,
           L.res_mode, L.z_out, L.obj_out, L.iters_out, L.tr_obj, L.tr_res, scratch,
-          work_global ? 1 : 0, L.fail);
+          work_global ? 1 : 0, L.fail, list, list_count, force_ref ? 1 : 0);
     }
   });
   err = cudaGetLastError();

@@ -94,6 +94,7 @@ constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 r
 constexpr int W_GR = W_NR + 8;  // [8] Gram row of the coming sweep: G[0..R-1], ||c~||^2, <m, c~>, ||c~_{t+1-R}||^2
 constexpr int W_TOTAL = W_GR + 8;
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
+constexpr int kProbe = 1024;  // pixels sampled by the small-mu probe launch
 constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
 constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2
 constexpr float kCancel = 1.0f / 256.0f;  // N below 2^-8 (H + ||c~||^2): the expansion cancels
@@ -308,7 +309,20 @@ using namespace lr;
 __global__ void __launch_bounds__(WARPS * 32, 1)
 nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, int out_row0,
                int plane, NlemDevParams P, float* out, float* frames, int* work_counter,
-               int* ovf_list, int* ovf_count, FailureSlot* fail) {
+               int* ovf_list, int* ovf_count, FailureSlot* fail, int probe_n, int* probe_count) {
+  // probe_n > 0 (probe launch): only the setup and the small-mu predictor of probe_n pixels
+  // spread evenly over the band, counting predicted hand-offs into *probe_count; no outputs.
+  // probe_n == 0 with probe_count (main launch): when more than 90 % of the probe pixels
+  // would be handed off (the small-mu regime), every pixel is: *ovf_count = -1 tells the tile
+  // kernel to take the whole band, and this launch does no pixel work.  The decision depends on
+  // the input only (deterministic).
+  if (probe_n == 0 && probe_count != nullptr) {
+    const int pt = plane < kProbe ? plane : kProbe;
+    if (10 * *static_cast<volatile int*>(probe_count) > 9 * pt) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) *ovf_count = -1;
+      return;
+    }
+  }
   extern __shared__ __align__(16) float smem[];
   // warp index through a shuffle: the compiler then knows it is warp-uniform (uniform datapath)
   const int warp = __shfl_sync(0xffffffffu, static_cast<int>(threadIdx.x >> 5), 0);
@@ -358,7 +372,13 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const bool irls = P.solver == NLEM_SOLVER_IRLS;
   const int total_warps = gridDim.x * WARPS;
 
-  int pix = blockIdx.x * WARPS + warp;
+  // work items: pixels, or (probe launch) probe_n samples at pixel i * plane / probe_n
+  const int nidx = probe_n ? probe_n : plane;
+  auto pix_of = [&](int i) {
+    return probe_n ? static_cast<int>(static_cast<long long>(i) * plane / probe_n) : i;
+  };
+  int idx = blockIdx.x * WARPS + warp;
+  int pix = pix_of(idx);
   auto issue_tile = [&](int p, int b) {
     const int r = out_row0 + p / cols, c = p % cols;
     const float* src = pad + static_cast<int64_t>(r - out_row0) * pad_cols + c;
@@ -390,13 +410,13 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     col[27] = 0.0f;
   }
   if (lane < SEGL + KS - 1) W[PB + 16 * PCS + 2 * lane + 1] = 0.0f;
-  if (pix < plane) issue_tile(pix, 0);
+  if (idx < nidx) issue_tile(pix, 0);
 
 #ifdef NLEM_LR_STAMPS
   long long st_t0 = 0, st_t1 = 0, st_t2 = 0, st_t3 = 0, st_wait = 0, st_setup = 0, st_sw = 0, st_epi = 0, st_n = 0;
   long long st_p[4] = {0, 0, 0, 0};
 #endif
-  while (pix < plane) {
+  while (idx < nidx) {
     int nxt = 0;
     if (lane == 0) nxt = atomicAdd(work_counter, 1) + total_warps;
     nxt = __shfl_sync(0xffffffffu, nxt, 0);
@@ -679,7 +699,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // sweeps - the pixel goes to the exact kernel right away.  A heuristic: a wrong guess costs
     // time, never accuracy.  Warp-uniform (gram[] holds the same value in every lane).
     if (P.iters > R && !static_eq && inv_mu * inv_mu >= gram[R]) ovf = true;
-    for (int t = 1; t <= P.iters && !ovf; ++t) {
+    for (int t = 1; t <= P.iters && !ovf && !probe_n; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
       float2 u[SEGL];  // ga' of (slot 0, slot 1): the FFMA2 pairs of the patch-sum pass
@@ -864,7 +884,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     st_t3 = clock64(); st_sw += st_t3 - st_t2;
 #endif
     const bool any_ovf = __any_sync(0xffffffffu, ovf);
-    if (any_ovf) {
+    if (probe_n) {
+      if (lane == 0 && any_ovf) atomicAdd(probe_count, 1);
+    } else if (any_ovf) {
       // a dropped history term would have been significant: the exact p-form kernel redoes it
       if (lane == 0) ovf_list[atomicAdd(ovf_count, 1)] = pix;
     } else if (ifail_iter >= 0) {
@@ -883,8 +905,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         for (int t = iters; t < P.iters; ++t) frames[static_cast<int64_t>(t) * plane + pix] = zc;
     }
     __syncwarp();  // every lane is done with the tile before the next one streams in
-    if (nxt < plane) issue_tile(nxt, 0);
-    pix = nxt;
+    if (nxt < nidx) issue_tile(pix_of(nxt), 0);
+    idx = nxt;
+    pix = pix_of(idx);
 #ifdef NLEM_LR_STAMPS
     { const long long e_ = clock64(); st_epi += e_ - st_t3; ++st_n; }
 #endif
@@ -910,19 +933,32 @@ bool nlem_lr_supported(const NlemLaunch& L) {
          L.out_rows * L.cols < lim && L.rows < lim && L.pad_cols < lim;
 }
 
+bool nlem_lr_probe_wanted(const NlemLaunch& L) {
+  return L.P.solver == NLEM_SOLVER_ADMM && L.P.iters > R;
+}
+
 cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
-                           cudaStream_t stream) {
+                           int* probe, cudaStream_t stream) {
   auto kfn = nlem_pixels_lr;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
   const int64_t pixels = L.out_rows * L.cols;
-  int64_t grid = device_caps().sms;
-  grid = std::max<int64_t>(1, std::min<int64_t>(grid, (pixels + WARPS - 1) / WARPS));
+  const int sms = device_caps().sms;
+  if (probe != nullptr) {  // probe[0] = predicted hand-offs, probe[1] = the probe's work counter
+    const int pn = static_cast<int>(std::min<int64_t>(pixels, kProbe));
+    const int64_t pgrid = std::max<int64_t>(1, std::min<int64_t>(sms, (pn + WARPS - 1) / WARPS));
+    kfn<<<static_cast<unsigned>(pgrid), WARPS * 32, SMEM_BYTES, stream>>>(
+        L.pad, static_cast<int>(L.pad_cols), static_cast<int>(L.rows), static_cast<int>(L.cols),
+        static_cast<int>(L.out_row0), static_cast<int>(pixels), L.P, L.out, L.frames, probe + 1,
+        ovf_list, ovf_count, L.fail, pn, probe);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(sms, (pixels + WARPS - 1) / WARPS));
   kfn<<<static_cast<unsigned>(grid), WARPS * 32, SMEM_BYTES, stream>>>(
       L.pad, static_cast<int>(L.pad_cols), static_cast<int>(L.rows), static_cast<int>(L.cols),
       static_cast<int>(L.out_row0), static_cast<int>(pixels), L.P, L.out, L.frames, counter,
-      ovf_list, ovf_count, L.fail);
+      ovf_list, ovf_count, L.fail, 0, probe);
   return cudaGetLastError();
 }
 

@@ -14,8 +14,6 @@
 #include <cstdlib>
 #include <cstring>
 
-#include <cooperative_groups.h>
-
 #include "launch.h"
 #include "solver_generic.cuh"
 
@@ -56,7 +54,7 @@ __device__ long long g_setup[64][8];  // thread 0 of CTA 0: per-pixel setup stam
 #ifndef NLEM_XW4_CPT
 #define NLEM_XW4_CPT 8
 #endif
-template <int KS_, int SW_, int KB_, int CL_, int XW_ = 0>
+template <int KS_, int SW_, int KB_, int XW_ = 0>
 struct TileCfg {
   static constexpr int KS = KS_;                 // patch side k
   static constexpr int SW = SW_;                 // search window side S
@@ -66,22 +64,18 @@ struct TileCfg {
   static constexpr int GPW = 32 / G;             // groups per warp
   static constexpr int NBLK = SW / KB;           // segments per grid row
   static constexpr int NGROUPS = SW * NBLK;
-  static constexpr int CL = CL_;                 // CTAs per pixel (thread-block cluster)
-  static constexpr int NGC = (NGROUPS + CL - 1) / CL;  // groups per CTA
+  static constexpr int NGC = NGROUPS;            // groups per CTA (one CTA per pixel)
   static constexpr int WARPS = (NGC + GPW - 1) / GPW;  // point warps
-  // consensus mode (CL == 1 only for 1, 2): 0 = CPT threads per coordinate over all warps
-  // between two CTA barriers; 1 = a dedicated extra consensus warp; 2 = the last point warp
-  // to hand in its partials (smem arrival counter) runs the consensus; 3 = each warp pre-reduces
-  // its groups' partials into one warp row, one CTA barrier, then the last warp alone runs the
-  // consensus over the warp rows while the others prepare the next sweep's state; 4 = warp
-  // pre-reduction, then CPT threads per coordinate over the warp rows (all warps), with the
-  // next sweep's state update issued between the consensus loads and their reduction
+  // consensus mode: 0 = CPT threads per coordinate over all warps between two CTA barriers
+  // (k = 5); 4 = split p-form: warp pre-reduction, then CPT threads per coordinate over the
+  // warp rows, with the next sweep's state update issued between the consensus loads and
+  // their reduction (k = 7)
   static constexpr int XW = XW_;
-  // split-form paths (XW >= 1) publish c as KS padded rows of CSTR floats so a lane reads its
-  // patch row with 128-bit loads; CSTR/4 odd keeps the 7 row reads of a warp conflict-free
+  // the split form publishes c as KS padded rows of CSTR floats so a lane reads its patch row
+  // with 128-bit loads; CSTR/4 odd keeps the 7 row reads of a warp conflict-free
   static constexpr int CSTR = (KS + 3) / 4 * 4 + ((((KS + 3) / 4) % 2) ? 0 : 4);
   static constexpr int CSN = (KS * CSTR + 3) & ~3;
-  static constexpr int THREADS = 32 * (WARPS + (XW == 1 ? 1 : 0));
+  static constexpr int THREADS = 32 * WARPS;
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
   static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
@@ -97,38 +91,29 @@ struct TileCfg {
   static constexpr int KSP = KS;                 // per-lane coordinate row (unpadded)
   // per-group block of g partials: D floats padded so that CPT consecutive-part blocks land
   // on disjoint bank quads (part * GSTR mod 32 in steps of 4): 52 for D = 49, CPT = 8
-  // (with a consensus warp, D = 49: 56 = the smallest even stride >= D + 2 whose row writes
-  // are conflict-free; the consensus warp's float2 row reads are conflict-free for any stride)
+  // (split form, D = 49: 56 = the smallest even stride >= D + 2 whose row writes are
+  // conflict-free)
   static constexpr int GSTR = (XW_ && D == 49) ? 56
                               : D == 49 ? 52 : ((D + 3) & ~3) + (((((D + 3) & ~3) / 4) % 2) ? 0 : 4);
-  // per-warp partial rows (XW >= 3): CPT4 = 8 threads read one coordinate from rows part, part+8,
+  // per-warp partial rows (split form): CPT4 = 8 threads read one coordinate from rows part, part+8,
   // ...; a stride of 52 puts the 8 parts on distinct bank quads (56 collided parts p, p+4)
   static constexpr int WSTR = D == 49 ? 52 : GSTR;
   static constexpr int SPL = (KB + G - 1) / G;   // points whose prox scale a lane computes
   static constexpr int CPT = THREADS >= 8 * D ? 8 : THREADS >= 4 * D ? 4 : THREADS >= 2 * D ? 2 : 1;
   static_assert(SW % KB == 0, "segments tile the grid row");
   static_assert(D <= THREADS, "consensus needs one thread per coordinate");
-  static_assert(XW == 0 || (CL == 1 && D <= 64), "consensus warp: one CTA, <= 2 coordinates per lane");
-  static_assert(XW != 2 || NGC <= 64, "arrival-counter consensus: 8 chains x 8 rows");
+  static_assert(XW == 0 || XW == 4, "consensus modes 0 and 4");
   // XW == 4: threads per coordinate of the consensus over the WARPS warp rows
   static constexpr int CPT4 = NLEM_XW4_CPT;
   static_assert(XW != 4 || (WARPS % CPT4 == 0 && CPT4 * D <= THREADS), "warp rows split evenly");
 };
 
-// configs 2, 3: 63 groups of 7 lanes split over a 2-CTA cluster (8 warps per CTA), so each
-// SM hosts halves of two pixels and one half's barrier/exchange latency overlaps the other's FP work
-#ifndef NLEM_TILE_CL
-#define NLEM_TILE_CL 1
-#endif
-// 1: one CTA per pixel (16 warps) — production.  2: pixel split over a 2-CTA cluster with a
-// DSMEM + mbarrier exchange per sweep — experimental: measured slower, the per-sweep exchange
-// waits ~1.2-1.7k cycles on skew between the two SMs (profiles/r1_tile_phase_times.txt)
-// dedicated consensus warp (1, production) or consensus spread over the point warps (0)
-#ifndef NLEM_TILE_XW
-#define NLEM_TILE_XW 4
-#endif
-using TileK7S21 = TileCfg<7, 21, 7, NLEM_TILE_CL, NLEM_TILE_CL == 1 ? NLEM_TILE_XW : 0>;
-using TileK5S11 = TileCfg<5, 11, 11, 1>;   // config 0: 11 groups of 5 lanes, 2 warps
+// k = 7 / S = 21 (configs 2, 3, 4; the hand-off target of the low-rank kernel): 63 groups of
+// 7 lanes, one CTA of 16 warps per pixel, split p-form.  (Round-1 experiments with a 2-CTA
+// cluster per pixel and with dedicated / last-arriving consensus warps measured slower,
+// profiles/r1_tile_phase_times.txt; they are not part of the build.)
+using TileK7S21 = TileCfg<7, 21, 7, 4>;
+using TileK5S11 = TileCfg<5, 11, 11, 0>;   // config 0: 11 groups of 5 lanes, 2 warps
 
 template <class C>
 struct TileSmem {
@@ -136,43 +121,16 @@ struct TileSmem {
   static constexpr int ROWS = C::NGC * C::G + 40;  // local groups + dummy rows for idle lanes
   static constexpr int NB = (ROWS * C::KBP + 3) & ~3;    // norm transpose (16-byte multiple)
   static constexpr int RED = ((C::NGC + 8) * C::GSTR + C::WARPS * C::WSTR + 3) & ~3;  // g partials per group
-                                                   // (+ dummy groups) and per warp (XW >= 3)
+                                                   // (+ dummy groups) and per warp (split form)
   static constexpr int TOTAL = 2 * T + NB + RED + C::CSN /*cs*/ + 2 * C::D /*c2*/ + 2 * C::D /*z, a0*/ +
-                               C::NGROUPS * C::KBP /*w*/ + 64 + 2 * (C::D + 8) /*cluster rx*/ +
-                               4 /*mbarrier*/;
+                               C::NGROUPS * C::KBP /*w*/ + 64;
 };
 
 __device__ __forceinline__ float2 tf2(float x) { return make_float2(x, x); }
 
-// --- cluster one-way exchange: DSMEM store + remote mbarrier arrive (release.cluster), local
-// parity wait (acquire.cluster).  Cheaper than a full cluster barrier: a consumer waits only
-// for the peer's producers, not for every thread of both CTAs.
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ uint32_t mapa_peer(uint32_t local, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_cluster_f32(uint32_t addr, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t addr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
-}
-__device__ __forceinline__ void mbar_wait_parity(uint32_t addr, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P1;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
-      " @!P1 bra WAIT_%=;\n}\n" ::"r"(addr),
-      "r"(parity)
-      : "memory");
-}
-constexpr int kExchArrivals = 50;
 
 __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(gsrc)
@@ -180,7 +138,7 @@ __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
-}  // 49 coordinate producers + thread 0 (flags / scalar)
+}
 __device__ __forceinline__ float rsqrt_ftz(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -190,13 +148,6 @@ __device__ __forceinline__ float2 tsub2(float2 a, float2 b) {
   return __fadd2_rn(a, make_float2(-b.x, -b.y));
 }
 __device__ __forceinline__ float2 tfma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
-// named CTA barriers (id 0 is __syncthreads): producers arrive without waiting
-__device__ __forceinline__ void named_bar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void named_bar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
 
 // Per-lane register image of its tile segment t[0..SEG): E[i] = (t[2i], t[2i+1]),
 // O[i] = (t[2i+1], t[2i+2]).  a_{m,dc} = t[m+dc].
@@ -221,27 +172,24 @@ struct TileCtx {
   float* T1;    // tile shifted left by one column
   float* nbuf;  // [NGROUPS][G][KBP]
   float* red;   // [NGC + 8][GSTR] per-group g partials
-  float* wred;  // [WARPS][GSTR] per-warp g partials (XW >= 3)
+  float* wred;  // [WARPS][WSTR] per-warp g partials (split form)
   float2* c2;   // [D]
-  float* cs;    // [KS][CSTR] c rows (XW >= 1)
+  float* cs;    // [KS][CSTR] c rows (split form)
   float* z;     // [D]
   float* a0;    // [D]
   float* wbuf;  // [NGROUPS][KBP]
   int* flags;   // [4]
   float* scal;  // [32]
-  float* rx;    // [2][D + 8] cluster receive buffers (partials from the peer CTA)
-  unsigned long long* mbar;  // cluster exchange mbarrier (arrivals from the peer CTA)
   int tid, warp, lane, q, dr, base;
   int grow0;    // first transpose/partial row of the lane's group (dummy rows if idle)
   bool active;  // lane belongs to a real group
   bool slot;    // lane belongs to a group slot (lanes past GPW * G of a warp are idle)
   int gr, gc0;  // grid row and first grid column of the lane's segment
 
-  int rank, nloc;  // CTA rank in the cluster, real groups held by this CTA
-  int xpar = 0;    // cluster exchange parity (double-buffered receive buffers)
+  int nloc;        // real groups (the pixel's 63 segments)
   int dbg_it = 0;  // debug phase-profile sweep counter
   int dbg_px = 0;  // debug setup-profile pixel counter
-  __device__ void carve(float* smem, int cta_rank) {
+  __device__ void carve(float* smem) {
     T0 = smem;
     T1 = T0 + TileSmem<C>::T;
     nbuf = T1 + TileSmem<C>::T;
@@ -254,19 +202,15 @@ struct TileCtx {
     wbuf = a0 + C::D;
     flags = reinterpret_cast<int*>(wbuf + C::NGROUPS * C::KBP);
     scal = reinterpret_cast<float*>(flags + 8);
-    rx = scal + 32;
-    mbar = reinterpret_cast<unsigned long long*>(
-        reinterpret_cast<uintptr_t>(rx + 2 * (C::D + 8) + 1) & ~uintptr_t(7));
     tid = threadIdx.x;
     warp = tid >> 5;
     lane = tid & 31;
     const int ql = lane / C::G;
     dr = lane - ql * C::G;
     base = ql * C::G;
-    rank = cta_rank;
-    const int lq = warp * C::GPW + ql;  // local group
-    q = rank * C::NGC + lq;             // global group
-    nloc = min(C::NGC, C::NGROUPS - rank * C::NGC);
+    const int lq = warp * C::GPW + ql;  // group
+    q = lq;
+    nloc = C::NGROUPS;
     active = ql < C::GPW && lq < nloc;
     slot = ql < C::GPW;
     // lanes of a group slot without a real group keep their slot's rows (all-zero partials, so
@@ -329,14 +273,11 @@ __device__ __forceinline__ void group_broadcast(const TileCtx<C>& X, const float
 
 // Sum the per-lane coordinate partials v[dc] (coordinate j = dr*KS + dc) over all groups:
 // lanes write red[lq][dr][dc]; after a barrier CPT threads per coordinate sum this CTA's
-// groups in a fixed order.  With a 2-CTA cluster the two partials are exchanged through
-// distributed shared memory (each CTA stores into the peer's receive buffer, one cluster
-// barrier) and combined as rank0 + rank1 in both CTAs, so both hold bitwise-identical
-// totals.  The local flag word flags[fslot] travels with the partials (OR-combined).
-// `finish(j, total)` runs on one thread per coordinate.  Ends with a CTA barrier.
+// groups in a fixed order.  `finish(j, total)` runs on one thread per coordinate.  Ends with a
+// CTA barrier.
 template <class C, class Finish>
 __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&v)[C::KS],
-                                                   int fslot, Finish finish) {
+                                                   Finish finish) {
   {
     float* row = X.red + (X.grow0 / C::G) * C::GSTR + X.dr * C::KS;  // idle lanes: dummy groups
 #pragma unroll
@@ -366,30 +307,6 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
 #pragma unroll
   for (int o = 1; o < C::CPT; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   PHASE(8);
-  if constexpr (C::CL == 2) {
-    const uint32_t peer = static_cast<uint32_t>(X.rank ^ 1);
-    const uint32_t rx_peer = mapa_peer(smem_u32(X.rx + X.xpar * (C::D + 8)), peer);
-    const uint32_t mb_peer = mapa_peer(smem_u32(X.mbar), peer);
-    if (j < C::D && part == 0) {
-      st_cluster_f32(rx_peer + 4u * j, s);
-      mbar_arrive_remote(mb_peer);
-    }
-    if (X.tid == 0) {
-      st_cluster_u32(rx_peer + 4u * C::D, static_cast<uint32_t>(X.flags[fslot]));
-      mbar_arrive_remote(mb_peer);
-    }
-    if ((j < C::D && part == 0) || X.tid == 0) mbar_wait_parity(smem_u32(X.mbar), X.xpar);
-    const float* own_rx = X.rx + X.xpar * (C::D + 8);
-    if (j < C::D && part == 0) {
-      const float o = own_rx[j];
-      s = X.rank == 0 ? s + o : o + s;
-    }
-    if (X.tid == 0) {
-      const int pf = reinterpret_cast<const int*>(own_rx)[C::D];
-      if (pf) atomicOr(&X.flags[fslot], pf);
-    }
-    X.xpar ^= 1;
-  }
   PHASE(11);
   if (j < C::D && part == 0) finish(j, s);
   PHASE(9);
@@ -398,54 +315,7 @@ __device__ __forceinline__ void reduce_coordinates(TileCtx<C>& X, const float (&
   PHASE(10);
 }
 
-// One warp's EM-ADMM consensus for sweep t (XW = 1, 2): lane l owns coordinates 2l, 2l+1 and
-// sums their float2 column over the local group rows in a fixed order (8 interleaved chains,
-// then a tree); z_t = P_C(z - g/n), c = 2 z_t - z (admm.hpp:59-65 in p-form); flag bits 4
-// (non-finite z) and 8 (z != a0, only if the exact-stop test is possible) into flags[t & 1];
-// clears flags[(t+1) & 1] (every read of sweep t-1's word is done).
-template <class C, int NR, int RSTR = C::GSTR>
-__device__ __forceinline__ void warp_consensus(TileCtx<C>& X, const float* rows, int t, float inv_n,
-                                               const nlem_box& range, bool static_eq) {
-  static_assert(RSTR % 2 == 0 && RSTR >= C::D + 1, "float2 coordinate pairs");
-  const int j = 2 * X.lane;
-  const bool own = j < C::D;
-  const float2* col = reinterpret_cast<const float2*>(rows + (own ? j : 0));
-  float2 ch[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) ch[i] = make_float2(0.0f, 0.0f);
-#pragma unroll
-  for (int g = 0; g < NR; ++g) {
-    const float2 v = col[g * (RSTR / 2)];
-    ch[g % 8] = g < 8 ? v : __fadd2_rn(ch[g % 8], v);
-  }
-#pragma unroll
-  for (int w = 1; w < 8; w <<= 1)
-#pragma unroll
-    for (int i = 0; i + w < 8; i += 2 * w) ch[i] = __fadd2_rn(ch[i], ch[i + w]);
-  int f = 0;
-  if (own) {
-    const float gs[2] = {ch[0].x, ch[0].y};
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int jj = j + e;
-      if (jj < C::D) {
-        const float zo = X.z[jj];
-        const float zn = clamp_box(fmaf(-gs[e], inv_n, zo), range);
-        f |= isfinite(zn) ? 0 : 4;
-        if (static_eq) f |= (zn != X.a0[jj]) ? 8 : 0;
-        X.z[jj] = zn;
-        X.cs[(jj / C::KS) * C::CSTR + jj % C::KS] = 2.0f * zn - zo;
-      }
-    }
-  }
-  f = __reduce_or_sync(0xffffffffu, f);
-  if (X.lane == 0) {
-    if (f) atomicOr(&X.flags[t & 1], f);
-    X.flags[(t + 1) & 1] = 0;
-  }
-}
-
-// IRLS consensus (CL == 1): lanes write their num partials v[dc] (coordinate j = dr*KS + dc)
+// IRLS consensus: lanes write their num partials v[dc] (coordinate j = dr*KS + dc)
 // and one lane per group writes the group's sum beta and sum w*root into columns D and D+1 of
 // the group row (GSTR >= D + 2).  CPT threads per coordinate sum the 3 columns over groups in
 // a fixed order; finish(j, num, den, sur) runs on one thread per coordinate.
@@ -498,54 +368,42 @@ __device__ __forceinline__ void irls_reduce(TileCtx<C>& X, const float (&v)[C::K
   __syncthreads();
 }
 
-// Cluster-wide sum of one scalar per lane (fixed order: warp tree, warps, rank0 + rank1).
+// CTA-wide sum of one scalar per lane (fixed order: warp tree, then warps).
 template <class C>
-__device__ __forceinline__ float cluster_sum_scalar(TileCtx<C>& X, float v) {
+__device__ __forceinline__ float block_sum_scalar(TileCtx<C>& X, float v) {
   v = warp_sum(v);
   if (X.lane == 0) X.scal[X.warp] = v;
   __syncthreads();
   float t = 0.0f;
 #pragma unroll
   for (int w = 0; w < C::WARPS; ++w) t += X.scal[w];
-  if constexpr (C::CL == 2) {
-    // same 50-arrival protocol as reduce_coordinates: threads 0..48 arrive, thread 0 twice
-    const uint32_t peer = static_cast<uint32_t>(X.rank ^ 1);
-    const uint32_t rx_peer = mapa_peer(smem_u32(X.rx + X.xpar * (C::D + 8)), peer);
-    const uint32_t mb_peer = mapa_peer(smem_u32(X.mbar), peer);
-    if (X.tid == 0) st_cluster_f32(rx_peer + 4u * (C::D + 1), t);
-    if (X.tid < kExchArrivals - 1) mbar_arrive_remote(mb_peer);
-    if (X.tid == 0) mbar_arrive_remote(mb_peer);
-    if (X.tid == 0) {
-      mbar_wait_parity(smem_u32(X.mbar), X.xpar);
-      const float o = X.rx[X.xpar * (C::D + 8) + C::D + 1];
-      X.scal[31] = X.rank == 0 ? t + o : o + t;
-    }
-    X.xpar ^= 1;
-    __syncthreads();
-    t = X.scal[31];
-  }
   __syncthreads();
   return t;
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, C::CL)
+__global__ void __launch_bounds__(C::THREADS, 1)
 nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
                  int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
                  int* work_counter, int chunk, FailureSlot* fail, const int* list,
                  const int* list_count) {
   extern __shared__ __align__(16) float smem[];
   TileCtx<C> X;
-  int crank = 0;
-  if constexpr (C::CL == 2) crank = static_cast<int>(cooperative_groups::this_cluster().block_rank());
-  X.carve(smem, crank);
-  __shared__ long long s_next_chunk[2];  // CL == 1: this CTA's next chunk (double-buffered)
+  X.carve(smem);
+  __shared__ long long s_next_chunk[2];  // this CTA's next chunk (double-buffered)
   int chunk_parity = 0;
   constexpr int hs = C::SW / 2;
   constexpr int center = C::D / 2;
   const int64_t plane = out_rows * cols;
   // list mode: only the listed band pixels (the low-rank kernel's hand-offs), in list order
-  const int64_t npix = list ? static_cast<int64_t>(*list_count) : plane;
+  // (a count of -1: the low-rank kernel handed off the whole band - the small-mu probe)
+  const int lcount = list ? *list_count : 0;
+  if (lcount < 0) {  // whole band: chunks of up to 8 pixels as in a direct launch
+    list = nullptr;
+    const int64_t c8 = plane / (static_cast<int64_t>(gridDim.x) * 4);
+    chunk = static_cast<int>(c8 < 1 ? 1 : c8 > 8 ? 8 : c8);
+  }
+  const int64_t npix = list ? static_cast<int64_t>(lcount) : plane;
   const int64_t nchunks = (npix + chunk - 1) / chunk;
   auto pixel_at = [&](int64_t q) -> int64_t { return list ? static_cast<int64_t>(list[q]) : q; };
   const float inv_mu = 1.0f / P.mu;
@@ -557,32 +415,18 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   const bool useT1E = !even, useT1O = even;
   // zero the tile slack columns once
   for (int e = X.tid; e < 2 * TileSmem<C>::T; e += C::THREADS) X.T0[e] = 0.0f;
-  if constexpr (C::CL == 2) {
-    if (X.tid == 0) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(X.mbar)),
-                   "r"(kExchArrivals));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    cooperative_groups::this_cluster().sync();  // peer's mbarrier initialised before use
-  }
   __syncthreads();
 
-  // pixel chunks: CL == 1 takes chunk blockIdx.x, then grabs the next one from a global
-  // counter at the start of each chunk (dynamic, so a slow SM does not stretch the launch);
-  // a 2-CTA cluster walks a static round-robin so both CTAs see the same pixels
-  const int64_t cid = blockIdx.x / C::CL, ncl = gridDim.x / C::CL;
+  // pixel chunks: a CTA takes chunk blockIdx.x, then grabs the next one from a global counter
+  // at the start of each chunk (dynamic, so a slow SM does not stretch the launch)
+  const int64_t cid = blockIdx.x, ncl = gridDim.x;
   int64_t prefetched = -1;  // pixel whose tile is already in flight to smem
   for (int64_t ch = cid; ch < nchunks;) {
     const int64_t q_end = (ch + 1) * chunk < npix ? (ch + 1) * chunk : npix;
-    if constexpr (C::CL == 1) {
-      // read after this chunk's first barrier; rewritten only after the chunk's last one
-      // (double-buffered: a slow reader of the previous slot can still be before its barrier)
-      if (X.tid == 0) s_next_chunk[chunk_parity] = ncl + atomicAdd(work_counter, 1);
-    }
-    const auto next_chunk = [&]() -> int64_t {
-      if constexpr (C::CL == 1) return s_next_chunk[chunk_parity];
-      return ch + ncl;
-    };
+    // read after this chunk's first barrier; rewritten only after the chunk's last one
+    // (double-buffered: a slow reader of the previous slot can still be before its barrier)
+    if (X.tid == 0) s_next_chunk[chunk_parity] = ncl + atomicAdd(work_counter, 1);
+    const auto next_chunk = [&]() -> int64_t { return s_next_chunk[chunk_parity]; };
     for (int64_t q = ch * chunk; q < q_end; ++q) {
       const int64_t pix = pixel_at(q);
       const int64_t r = out_row0 + pix / cols, c = pix % cols;
@@ -620,7 +464,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         X.flags[0] = 0;
         X.flags[1] = 0;
         X.flags[2] = 0;
-        X.flags[3] = 0;           // consensus arrival counter (XW == 2)
+        X.flags[3] = 0;
         X.flags[4] = 0x7fffffff;  // XW == 4: first failing sweep (2 t + [no non-finite z])
       }
       // ---- segment registers
@@ -683,7 +527,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       // ---- initial patch (nlem.cpp:13-18)
       const bool nlm_init = P.solver == NLEM_SOLVER_NLM_ONLY || P.init_mode == NLEM_INIT_NLM_PATCH;
       bool init_done = false;
-      if constexpr (C::CL == 1) {
+      {
         if (nlm_init) {
           // sum_k w_k a_k / sum_k w_k with the weight sum riding along as an extra consensus
           // column (one reduction, no separate W pass); algebraically the reference's
@@ -713,7 +557,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
         float wsum = 0.0f;
 #pragma unroll
         for (int i = 0; i < C::SPL; ++i) wsum += wown[i];
-        const float W = cluster_sum_scalar<C>(X, X.active ? wsum : 0.0f);
+        const float W = block_sum_scalar<C>(X, X.active ? wsum : 0.0f);
         const bool ratio = P.nlm_ratio != 0;
         float coef[C::KB];
 #pragma unroll
@@ -729,7 +573,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           if (C::ODD) t = fmaf(coef[C::KB - 1], S.single(dc), t);
           v[dc] = X.active ? t : 0.0f;
         }
-        reduce_coordinates<C>(X, v, 2, [&](int j, float tsum) { X.z[j] = ratio ? tsum / W : tsum; });
+        reduce_coordinates<C>(X, v, [&](int j, float tsum) { X.z[j] = ratio ? tsum / W : tsum; });
       } else {
         if (X.tid < C::D) {
           const int jr = X.tid / C::KS, jc = X.tid - jr * C::KS;
@@ -759,7 +603,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
       }
       SSTAMP(5);
       int iters = P.iters, fail_iter = -1, fail_kind = 0;
-      if constexpr (C::CL == 1) {
+      {
         if (P.solver == NLEM_SOLVER_IRLS) {
           // ---- IRLS on the smooth surrogate (proj/include/nlem/irls.hpp:21-68): pass p
           // evaluates at x_p: surrogate S(x_p) and beta_k = w_k / sqrt(||x_p - a_k||^2 + eps),
@@ -871,17 +715,17 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           __syncthreads();
         }
       }
-      if constexpr (C::XW >= 1) {
+      if constexpr (C::XW == 4) {
         if (P.solver == NLEM_SOLVER_ADMM) {
-          // ---- EM-ADMM sweeps, split p-form with a dedicated consensus warp.  Between sweeps
-          // a lane keeps q_k = s_k p_k - a_k; sweep t forms p_k = q_k + c (c = 2 z_{t-1} - z_{t-2}),
-          // the norms, prox scales and g partials (the critical path), hands the partials in
-          // with a non-blocking barrier arrive, and computes the next q while the consensus
-          // warp reduces the partials and publishes z_t and c.  Same iterates as the p-form
-          // (p' = s p + (c - a)) up to FP32 rounding order.
+          // ---- EM-ADMM sweeps, split p-form.  Between sweeps a lane keeps q_k = s_k p_k - a_k;
+          // sweep t forms p_k = q_k + c (c = 2 z_{t-1} - z_{t-2}), the norms, prox scales and g
+          // partials (the critical path), folds its warp's group rows, and after one barrier
+          // CPT4 threads per coordinate reduce the warp rows and publish z_t and c, with the
+          // next q computed between the consensus loads and their reduction.  Same iterates as
+          // the p-form (p' = s p + (c - a)) up to FP32 rounding order.
           if (X.tid < C::D) X.cs[(X.tid / C::KS) * C::CSTR + X.tid % C::KS] = X.z[X.tid];
           __syncthreads();
-          if (X.warp < C::WARPS) {
+          {
             float lam_own[C::SPL];
 #pragma unroll
             for (int i = 0; i < C::SPL; ++i) lam_own[i] = inv_mu * wown[i];
@@ -969,7 +813,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
               }
               if (fbits) {  // rare
                 atomicOr(&X.flags[t & 1], fbits);
-                if (C::XW == 4 && (fbits & 1)) atomicMin(&X.flags[4], 2 * t + 1);
+                if (fbits & 1) atomicMin(&X.flags[4], 2 * t + 1);
               }
               WSTAMP(1);
               // next sweep's q = s p - a (overlaps the consensus)
@@ -986,12 +830,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   for (int dc = 0; dc < C::KS; ++dc) p1[dc] = fmaf(s1, p1[dc], -S.single(dc));
                 }
               };
-              if constexpr (C::XW == 1) {
-                named_bar_arrive(1, C::THREADS);
-                q_update();
-                WSTAMP(2);
-                named_bar_sync(2, C::THREADS);
-              } else if constexpr (C::XW >= 3) {
+              {
                 // fold this warp's GPW group rows into its warp row (fixed order)
                 __syncwarp();
                 if (X.lane < (C::D + 1) / 2) {
@@ -1003,7 +842,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   reinterpret_cast<float2*>(X.wred + X.warp * C::WSTR)[X.lane] = acc;
                 }
                 __syncthreads();
-                if constexpr (C::XW == 4) {
+                {
                   // CPT threads per coordinate; loads first, then the state update, then the
                   // fixed-order reduction (rows part, part + CPT, ...) and the finish
                   constexpr int NPER = C::WARPS / C::CPT4;
@@ -1034,36 +873,6 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                   }
                   WSTAMP(2);
                   __syncthreads();
-                } else if (X.warp == C::WARPS - 1) {
-                  warp_consensus<C, C::WARPS, C::WSTR>(X, X.wred, t, inv_n, P.range, static_eq);
-                  __syncwarp();
-                  named_bar_arrive(2, C::THREADS);
-                  q_update();
-                } else {
-                  q_update();
-                  WSTAMP(2);
-                  named_bar_sync(2, C::THREADS);
-                }
-              } else {
-                // arrival counter: the warp that hands in the last partials runs the consensus
-                // and releases the others (named barrier 2: they sync, it arrives)
-                __threadfence_block();
-                __syncwarp();
-                int old = 0;
-                if (X.lane == 0) old = atomicAdd(&X.flags[3], 1);
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old == C::WARPS - 1) {
-                  __threadfence_block();
-                  warp_consensus<C, C::NGC>(X, X.red, t, inv_n, P.range, static_eq);
-                  if (X.lane == 0) X.flags[3] = 0;
-                  __threadfence_block();
-                  __syncwarp();
-                  named_bar_arrive(2, C::THREADS);
-                  q_update();
-                } else {
-                  q_update();
-                  WSTAMP(2);
-                  named_bar_sync(2, C::THREADS);
                 }
               }
               WSTAMP(3);
@@ -1071,7 +880,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 #ifdef NLEM_PHASE_PROFILE
               ++X.dbg_it;
 #endif
-              if constexpr (C::XW == 4) {
+              {
                 // failures are recorded as the first failing sweep (flags[4]) and decoded after
                 // the loop: no per-sweep flag read or divergent branch on the critical path; the
                 // flag word is read only when the exact-stop test is possible (constant footprint)
@@ -1085,22 +894,9 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                     break;
                   }
                 }
-              } else {
-                const int fl = X.flags[t & 1];
-                if (fl & (4 | 1)) {
-                  fail_iter = (fl & 4) || t == 1 ? t : t - 1;
-                  fail_kind = NLEM_FAIL_ADMM_ITERATE;
-                  break;
-                }
-                if (frames && X.tid == 0)
-                  frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
-                if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
-                  iters = t;
-                  break;
-                }
               }
             }
-            if constexpr (C::XW == 4) {
+            {
               // decode the first failure: non-finite z at sweep t -> t; a non-finite norm at
               // sweep t (multiplier blow-up in t - 1) -> t - 1, or t for t = 1
               const int fw = X.flags[4];
@@ -1109,23 +905,6 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
                 fail_iter = !(fw & 1) || tf == 1 ? tf : tf - 1;
                 fail_kind = NLEM_FAIL_ADMM_ITERATE;
               }
-            }
-          } else {
-            // dedicated consensus warp (XW == 1)
-            for (int t = 1; t <= P.iters; ++t) {
-              WSTAMP(0);
-              named_bar_sync(1, C::THREADS);
-              WSTAMP(1);
-              warp_consensus<C, C::NGC>(X, X.red, t, inv_n, P.range, static_eq);
-              __syncwarp();
-              const int fl = X.flags[t & 1];
-              WSTAMP(2);
-              named_bar_arrive(2, C::THREADS);
-#ifdef NLEM_PHASE_PROFILE
-              ++X.dbg_it;
-#endif
-              if (fl & (4 | 1)) break;
-              if (static_eq && !(fl & 2) && !(fl & 8)) break;
             }
           }
         }
@@ -1215,7 +994,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
           if (X.lane == 0 && fbits) atomicOr(&X.flags[t & 1], fbits);
           PHASE(4);
           // consensus z_t = P_C(z - g/n), c = 2 z_t - z  (admm.hpp:59-65 in p-form)
-          reduce_coordinates<C>(X, v, t & 1, [&](int j, float gsum) {
+          reduce_coordinates<C>(X, v, [&](int j, float gsum) {
             const float zo = X.z[j];
             const float zn = clamp_box(fmaf(-gsum, inv_n, zo), P.range);
             int f = isfinite(zn) ? 0 : 4;
@@ -1235,7 +1014,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
             fail_kind = NLEM_FAIL_ADMM_ITERATE;
             break;
           }
-          if (frames && X.tid == 0 && X.rank == 0)
+          if (frames && X.tid == 0)
             frames[static_cast<int64_t>(t - 1) * plane + pix] = X.z[center];
           if (static_eq && !(fl & 2) && !(fl & 8)) {  // residual exactly 0 (admm.hpp:77)
             iters = t;
@@ -1247,7 +1026,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
 #ifdef NLEM_PHASE_PROFILE
       ++X.dbg_px;
 #endif
-      if (X.tid == 0 && X.rank == 0) {
+      if (X.tid == 0) {
         if (fail_iter >= 0) {
           record_failure(fail, r * cols + c, fail_iter, fail_kind);
         } else {
@@ -1265,8 +1044,6 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
     ch = next_chunk();
     chunk_parity ^= 1;
   }
-  // no CTA may exit while its peer can still store into its shared memory
-  if constexpr (C::CL == 2) cooperative_groups::this_cluster().sync();
 }
 
 namespace {
@@ -1280,40 +1057,21 @@ cudaError_t launch_tile(const NlemLaunch& L, cudaStream_t stream, const int* lis
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int64_t pixels = L.out_rows * L.cols;
-  cudaLaunchConfig_t cfg = {};
-  cudaLaunchAttribute attr[1];
-  cfg.blockDim = dim3(C::THREADS);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = stream;
-  int64_t clusters = 1;
-  if constexpr (C::CL > 1) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = C::CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cfg.gridDim = dim3(C::CL * 148);
-    int ncl = 0;
-    e = cudaOccupancyMaxActiveClusters(&ncl, kfn, &cfg);
-    if (e != cudaSuccess) return e;
-    clusters = std::max(ncl, 1);
-  } else {
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
-    clusters = int64_t(device_caps().sms) * std::max(per_sm, 1);
-  }
-  const int chunk = list ? 1 : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (clusters * 4))));
-  clusters = std::max<int64_t>(1, std::min<int64_t>(clusters, (pixels + chunk - 1) / chunk));
-  cfg.gridDim = dim3(static_cast<unsigned>(clusters * C::CL));
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, C::THREADS, smem);
+  int64_t ctas = int64_t(device_caps().sms) * std::max(per_sm, 1);
+  const int chunk = list ? 1 : static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, pixels / (ctas * 4))));
+  ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (pixels + chunk - 1) / chunk));
   int* counter = nullptr;  // dynamic chunk counter (stream-ordered scratch)
   e = cudaMallocAsync(&counter, sizeof(int), stream);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(counter, 0, sizeof(int), stream);
-  if (e == cudaSuccess)
-    e = cudaLaunchKernelEx(&cfg, kfn, L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows,
-                           L.P, L.out, L.frames, counter, chunk, L.fail, list, list_count);
-  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    kfn<<<static_cast<unsigned>(ctas), C::THREADS, smem, stream>>>(
+        L.pad, L.pad_cols, L.rows, L.cols, L.out_row0, L.out_rows, L.P, L.out, L.frames, counter,
+        chunk, L.fail, list, list_count);
+    e = cudaGetLastError();
+  }
   const cudaError_t ef = cudaFreeAsync(counter, stream);
   return e != cudaSuccess ? e : ef;
 }
@@ -1335,7 +1093,6 @@ namespace nlemk {
 #endif
 
 bool nlem_tile_supported(const NlemLaunch& L) {
-  if (L.P.solver == NLEM_SOLVER_IRLS && TileK7S21::CL != 1 && L.P.patch == 7) return false;
   return (L.P.patch == 7 && L.P.search == 21) || (L.P.patch == 5 && L.P.search == 11);
 }
 

@@ -79,7 +79,12 @@ struct NlemLaunch {
   FailureSlot* fail;
 };
 
-cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream);
+// list / list_count (device): only the listed problems; force_ref: reference-form sweep
+cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream, const int* list = nullptr,
+                                const int* list_count = nullptr, bool force_ref = false);
+// Collinear point sets (affine rank 1, not all equal): appends problem indices to list
+cudaError_t launch_collinear(const float* points, int64_t batch, int n, int d, int* list,
+                             int* count, cudaStream_t stream);
 cudaError_t launch_irls_generic(const IrlsLaunch& L, cudaStream_t stream);
 cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t rows, int64_t cols,
                             float* pad, int64_t pad_row0, int64_t pad_rows, int64_t pad_cols,
@@ -97,7 +102,9 @@ cudaError_t launch_admm_fast_list(const AdmmLaunch& L, const int* list, const in
 // finish exactly (ring overflow, all points equal, non-finite values) are appended to ho_list
 // for launch_admm_fast_list.
 bool admm_lr_supported(const AdmmLaunch& L);
-cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, cudaStream_t stream);
+// probe: NULL or one zeroed int (small-mu probe launch before the main one)
+cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int* probe,
+                           cudaStream_t stream);
 // Register-resident batched IRLS for d = 49 (kernels_batched_lr.cu).
 bool irls_reg_supported(const IrlsLaunch& L);
 cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream);
@@ -110,8 +117,11 @@ bool nlem_fast_supported(const NlemLaunch& L);
 // Low-rank (Gram-form) one-pixel-per-warp kernel (kernels_nlem_lr.cu): pixels whose history
 // ring would drop a significant term are appended to ovf_list for the tile kernel.
 bool nlem_lr_supported(const NlemLaunch& L);
+// probe: NULL, or 2 zeroed ints for the small-mu probe launch (nlem_lr_probe_wanted); when the
+// probe predicts the whole band is handed off, *ovf_count becomes -1 (= every pixel)
+bool nlem_lr_probe_wanted(const NlemLaunch& L);
 cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
-                           cudaStream_t stream);
+                           int* probe, cudaStream_t stream);
 cudaError_t launch_nlem_fast(const NlemLaunch& L, cudaStream_t stream);
 
 cudaError_t launch_frames_sse(const float* frames, const float* clean, int64_t nframes,

@@ -102,8 +102,8 @@ constexpr int kRefFormMaxDim = 16;
 __host__ __device__ inline bool use_ref_form(int n, int d) { return n <= 2 || d <= kRefFormMaxDim; }
 
 // floats of solver state per problem (p-form: p; reference form: x and y)
-__host__ __device__ inline size_t admm_state_floats(int n, int d) {
-  return static_cast<size_t>(n) * d * (use_ref_form(n, d) ? 2 : 1);
+__host__ __device__ inline size_t admm_state_floats(int n, int d, bool force_ref = false) {
+  return static_cast<size_t>(n) * d * (force_ref || use_ref_form(n, d) ? 2 : 1);
 }
 
 // Reference-form block sweep (admm.hpp:49-78 in float): state y (multipliers) and x
@@ -242,9 +242,9 @@ template <int JPL, class OnIter>
 __device__ SolveStatus admm_solve_generic(const float* a, const float* w, float* p, int n, int d,
                                           GenWork& W, nlem_box box, float mu, int T, float tol,
                                           int res_mode, float* trace_obj, float* trace_res,
-                                          OnIter on_iter) {
+                                          OnIter on_iter, bool force_ref = false) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (use_ref_form(n, d))
+  if (force_ref || use_ref_form(n, d))
     return admm_solve_refform<JPL>(a, w, p + static_cast<size_t>(n) * d, p, n, d, W, box, mu, T,
                                    res_mode == RES_NONE ? -1.0f : tol, trace_obj, trace_res,
                                    on_iter);

@@ -79,3 +79,41 @@ def test_two_rank_bands_match_single_process(tmp_path, oracle, world):
     ref = oracle.nlem_denoise(noisy.astype(np.float64), p).astype(np.float32)
     assert got.shape == ref.shape
     assert (got == ref).all()
+
+
+def _gpu_worker(rank, world, port, noisy, out_path):
+    sys.path.insert(0, ROOT)
+    import torch.distributed as dist
+
+    import paper_1501_03879_b200 as nb
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = nb.NlemParams(search=21, patch=7, h=10 * 20.0 * 7, sigma=20.0, solver="admm",
+                      solver_iters=10, mu=1.0, init_mode="nlm")
+    # every rank on device 0 (one GPU here); each band goes through the host-buffer C-ABI
+    res = D.denoise_bands(noisy, 21, 7, rank, world, D.gpu_band_fn(p, device=0))
+    if rank == 0:
+        np.save(out_path, res)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_gpu_bands_over_ranks_match_single_call(tmp_path, world):
+    """The multi-GPU row-band path with the GPU band function (dist.gpu_band_fn ->
+    nlem_denoise_rows_host): world ranks (gloo, all on cuda:0 here), each with its own band
+    and 13-row halo, gathered on rank 0 - bitwise equal to one whole-image call."""
+    import paper_1501_03879_b200 as nb
+    from paper_1501_03879_b200 import synth
+
+    _, noisy = synth.noisy_image(77, 64, 10, 6, 20.0)
+    out_path = str(tmp_path / "out.npy")
+    mp.spawn(_gpu_worker, args=(world, _free_port(), noisy, out_path), nprocs=world, join=True)
+    got = np.load(out_path)
+    p = nb.NlemParams(search=21, patch=7, h=10 * 20.0 * 7, sigma=20.0, solver="admm",
+                      solver_iters=10, mu=1.0, init_mode="nlm")
+    ref = nb.nlem_denoise_host(noisy, p)
+    assert got.shape == ref.shape and np.array_equal(got, ref)

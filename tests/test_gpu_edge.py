@@ -46,3 +46,44 @@ def test_huge_search_window_vs_oracle(nb, oracle):
     out = nb.nlem_denoise(img, g)
     ref = oracle.nlem_denoise(img.astype(np.float64), o)
     assert np.abs(out - ref).max() <= 1e-2
+
+
+@pytest.mark.parametrize("d", [25, 30, 49])
+def test_collinear_point_sets_exact_stop(nb, oracle, d):
+    """Collinear point sets (a_k = a_0 + t_k v) are one-dimensional: with tol 0 the reference's
+    exact-zero residual stop (admm.hpp:77) is reachable there.  The three-point case of the
+    advisor (+-1 in one coordinate, w = 1, mu = 1) stops at iteration 2 in the FP64 oracle;
+    the GPU must report the same count for every collinear problem of a batch that also holds
+    generic problems (d = 25: fast kernel, 30: generic p-form, 49: low-rank kernel)."""
+    rng = np.random.default_rng(d)
+    probs, ws = [], []
+    base = rng.integers(20, 200, d).astype(np.float32)
+    e = np.zeros(d, np.float32)
+    e[d // 3] = 1.0
+    probs.append(np.stack([base, base + e, base - e]))
+    ws.append(np.ones(3, np.float32))
+    n = 3
+    v = rng.integers(-3, 4, d).astype(np.float32)
+    for b in range(5):
+        if b % 2 == 0:  # collinear along v with small integer steps (exact in float)
+            t = rng.integers(-6, 7, n).astype(np.float32)
+            probs.append(base[None] + t[:, None] * v[None])
+        else:  # generic
+            probs.append(rng.uniform(0, 255, (n, d)).astype(np.float32))
+        ws.append(np.ones(n, np.float32))
+    pts = np.stack(probs)
+    w = np.stack(ws)
+    for mu in (1.0, 0.5):
+        r = nb.admm_euclidean_median(pts, w, nb.BoxConstraint.unconstrained(),
+                                     nb.AdmmConfig(mu=mu, max_iter=50))
+        ref = oracle.admm_batched(pts.astype(np.float64), w.astype(np.float64), mu=mu, max_iter=50)
+        # the +-1 three-point case: the same exact-stop sweep as the FP64 reference
+        assert r.iterations_run[0] == ref.iterations[0] < 50, (r.iterations_run, ref.iterations)
+        # generic problems never stop exactly
+        assert (r.iterations_run[[2, 4]] == 50).all() and (ref.iterations[[2, 4]] == 50).all()
+        assert np.abs(r.minimizer[[0, 2, 4]] - ref.minimizer[[0, 2, 4]]).max() <= 1e-3
+        # the other collinear sets stop early too, but an exactly-zero residual is a rounding
+        # event there: the sweep at which FP32 and FP64 reach it can differ (as for d <= 16,
+        # where test_random_instances_vs_oracle excludes such tie problems from the comparison)
+        early = ref.iterations < 50
+        assert (r.iterations_run[early] < 50).all(), (r.iterations_run, ref.iterations)

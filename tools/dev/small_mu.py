@@ -31,3 +31,24 @@ for mu in (1.0, 1e-3):
     t = min(ts[1:])
     print(f"kernel={os.environ.get('NLEM_KERNEL', 'prod')} mu={mu} rows={rows}: {t:.2f} ms "
           f"= {rows * 4096 / t / 1e3:.2f} Mpix/s sum={float(out.double().sum()):.6f}", flush=True)
+
+# config 1 (batched standalone solves, n = 441, d = 49, T = 50) at mu = 1 and mu = 1e-3
+import numpy as np  # noqa: E402
+
+B = 16384
+pts, w = synth.point_sets(B)
+P, Wt = torch.from_numpy(pts).cuda(), torch.from_numpy(w).cuda()
+for mu in (1.0, 1e-3):
+    cfg = nb.AdmmConfig(mu=mu, max_iter=50)
+    box = nb.BoxConstraint.interval(0.0, 255.0)
+    ts = []
+    for i in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record()
+        r = nb.admm_euclidean_median(P, Wt, box, cfg)
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    t = min(ts[1:])
+    print(f"config1 mu={mu} B={B}: {t:.2f} ms = {B / t / 1e3:.3f} M problems/s", flush=True)
