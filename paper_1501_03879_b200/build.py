@@ -46,22 +46,9 @@ def _stale() -> bool:
 
 # experimental build variants (A/B and debug only): "_"-separated tokens -> defines
 _VARIANT_TOKENS = {
-    "prof": "-DNLEM_PHASE_PROFILE",  # clock64 phase stamps (nlem_debug_phase_times)
-    "blrst": "-DNLEM_BLR_STAMPS",
-    "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-pixel phase clock64 sums (printf)    # batched low-rank kernel: per-phase clock64 sums (printf)
-    "cl2": "-DNLEM_TILE_CL=2",       # 2-CTA cluster tile kernel
-    "xw0": "-DNLEM_TILE_XW=0",       # consensus spread over the point warps
-    "xw1": "-DNLEM_TILE_XW=1",       # dedicated consensus warp
-    "xw2": "-DNLEM_TILE_XW=2",       # last-arriving warp runs the consensus
-    "xw3": "-DNLEM_TILE_XW=3",       # warp pre-reduction + one consensus warp
-    "xw4": "-DNLEM_TILE_XW=4",       # warp pre-reduction + CPT consensus, split p-form
-    "lrw12": "-DNLEM_LR_WARPS=12",   # low-rank kernel with 12 pixel-warps per SM (168 registers)
-    "lrw14": "-DNLEM_LR_WARPS=14",
-    "ud1": "-DNLEM_LR_UD=1",         # low-rank kernel: rolled dot-product column loop (default 7)
-    "ug4": "-DNLEM_LR_UG=4",         # low-rank kernel: unrolled patch-sum column loop
-    "st1": "-DNLEM_LR_ST=1",         # low-rank kernel: columns per TMEM store in the sweep
-    "st4": "-DNLEM_LR_ST=4",
-    "cpt1": "-DNLEM_XW4_CPT=1",      # XW=4 consensus threads per coordinate
+    "prof": "-DNLEM_PHASE_PROFILE",  # tile kernel: clock64 phase stamps (nlem_debug_phase_times)
+    "blrst": "-DNLEM_BLR_STAMPS",    # batched low-rank kernel: per-phase clock64 sums (printf)
+    "cpt1": "-DNLEM_XW4_CPT=1",      # tile kernel: consensus threads per coordinate
     "cpt2": "-DNLEM_XW4_CPT=2",
     "cpt4": "-DNLEM_XW4_CPT=4",
     "cpt8": "-DNLEM_XW4_CPT=8",
@@ -80,12 +67,14 @@ def build(force: bool = False, verbose: bool = False, variant: str = "") -> str:
     os.makedirs(OUT_DIR, exist_ok=True)
     toks = [t for t in variant.split("_") if t]
     extra = [_VARIANT_TOKENS[t] for t in toks if t in _VARIANT_TOKENS]
-    # "lrr1": A/B against the round-1 image kernel (tools/dev/kernels_nlem_lr_r1.cu)
+    # A/B against saved image-kernel versions (tools/dev/kernels_nlem_lr_*.cu): "lrr1" = round 1,
+    # "lrnp2" = the rejected two-pixels-per-warp template (profiles/r2_np2_experiment.txt)
     swap = {}
-    if "lrr1" in toks:
-        swap[os.path.join(CSRC, "kernels_nlem_lr.cu")] = os.path.join(
-            os.path.dirname(HERE), "tools", "dev", "kernels_nlem_lr_r1.cu")
-        extra += ["-I", CSRC]
+    for tok, fname in (("lrr1", "kernels_nlem_lr_r1.cu"), ("lrnp2", "kernels_nlem_lr_np2_experiment.cu")):
+        if tok in toks:
+            swap[os.path.join(CSRC, "kernels_nlem_lr.cu")] = os.path.join(
+                os.path.dirname(HERE), "tools", "dev", fname)
+            extra += ["-I", CSRC]
     tag = f"_{variant}" if variant else ""
     jobs = []
     for src in sources():
