@@ -124,34 +124,32 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def load_profile_traffic():
-    """dram bytes per launch of the dominant kernel from the committed ncu summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+def load_profile_summary():
+    """The committed ncu summary of the dominant kernel (profiles/ncu_summary.json)."""
     try:
-        with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f)
     except Exception:
-        return None
+        return {}
 
 
-def load_profile_pipes():
-    """Executed-work utilisation of the dominant kernel (committed ncu summary): explains a
-    roofline fraction above 1 (the algorithmic count exceeds the low-rank form's executed work)."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    try:
-        with open(p) as f:
-            d = json.load(f)
-        return {"fma_pipe_active_pct": d.get("fma_pipe_active_pct"),
-                "issue_active_pct": d.get("issue_active_pct"),
-                "smem_wavefronts_pct": d.get("smem_wavefronts_pct"), "source": d.get("pipe_source"),
-                "note": "frac is algorithmic: 12 flops per (pixel, neighbour, coordinate, sweep) "
-                        "as SURVEY.md 8(d) counts Algorithm 1; the low-rank (Gram-form) kernel "
-                        "executes about a third of them, so frac can exceed 1 while the FP32 pipe "
-                        "is busy fma_pipe_active_pct of the time; the shared-memory data pipe "
-                        "(tile column loads of the correlation / patch-sum loops) runs at "
-                        "smem_wavefronts_pct and instruction issue at issue_active_pct: co-limits"}
-    except Exception:
+def executed_block(summary, mpix_per_s, peak):
+    """Executed FP32 work next to the algorithmic count: the low-rank kernel executes fewer
+    flops than Algorithm 1's 12 per (point, coordinate, sweep), so the algorithmic fraction can
+    exceed 1; the executed fraction and the pipe utilisations are the hardware view."""
+    fpp = summary.get("executed_fp32_flops_per_pixel")
+    if not fpp:
         return None
+    tf = fpp * mpix_per_s * 1e6 / 1e12
+    return {"fp32_tflops_executed": tf, "frac_executed": tf / peak,
+            "executed_flops_per_pixel": fpp,
+            "fma_pipe_active_pct": summary.get("fma_pipe_active_pct"),
+            "issue_active_pct": summary.get("issue_active_pct"),
+            "smem_wavefronts_pct": summary.get("smem_wavefronts_pct"),
+            "source": summary.get("executed_source"),
+            "note": "executed = ncu-counted FP32 instructions per pixel (FFMA2 4 flops, FADD2 / "
+                    "FMUL2 / FFMA 2, FADD / FMUL 1 per thread) x this run's pixel rate; the FMA "
+                    "pipe, instruction issue and the shared-memory data pipe are co-limits"}
 
 
 def bench_config(gpus: int) -> dict:
@@ -428,6 +426,7 @@ def main():
                              "configs[1] (65,536 x n=441 x d=49, T=50, mu=1), config 2 = 512^2")
 
     value = rows * cols / (total_ms / args.steps / 1e3) / 1e6
+    summary = load_profile_summary()
     e2e_val = rows * cols / (e2e_s / args.steps) / 1e6
     clk = clocks.summary()
     peak = PEAK_FP32_TFLOPS_NOMINAL
@@ -439,25 +438,34 @@ def main():
         "config": config,
         "roofline": {"bound": "fp32", "achieved": float(achieved_t.item()), "peak": peak,
                      "unit": "TFLOP/s", "frac": float(achieved_t.item()) / peak,
-                     "traffic": load_profile_traffic(),
-                     "executed": load_profile_pipes(),
+                     "traffic": summary.get("dram_bytes_per_launch"),
+                     "executed": executed_block(summary, value, peak),
                      "peak_source": "derived 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (no FP32 "
-                                    "figure in MEASURED_PEAKS.json)",
-                     "kernel": "nlem pixel kernel (+pad), per-step CUDA events",
+                                    "figure in MEASURED_PEAKS.json); measured FFMA2 issue rate "
+                                    f"{summary.get('peak_ffma2_tflops_measured')} TFLOP/s "
+                                    "(profiles/r2_fp32_peak.txt)",
+                     "kernel": "nlem pixel kernel (+validate, pad, probe, hand-off), per-step "
+                               "CUDA events",
                      "algorithmic_flops_per_step": flops,
+                     "algorithmic_count": "12 d T sum_n (ADMM) + 3 d sum_n (weights) + 2 d sum_n "
+                                          "(NLM init), SURVEY.md 8(d)",
                      "frac_at_measured_clock": (float(achieved_t.item()) / peak *
                                                 (clk["sm_max_mhz"] / clk["sm_mhz"])
                                                 if clk.get("sm_mhz") and clk.get("sm_max_mhz")
-                                                else None)},
+                                                else None),
+                     "tile_staging": "4-byte cp.async into the paired smem layout, not TMA: TMA "
+                                     "has no mirror mode and needs 16-byte-aligned box starts; a "
+                                     "TMA box prefetch measured 2 % slower "
+                                     "(tools/dev/tma_tile_experiment.patch)"},
         "cpu_baseline": cpu,
         "parity": parity,
         "e2e": {"value": e2e_val, "unit": "Mpixels/s",
                 "h2d_bytes_per_step": int(band_in.nbytes), "d2h_bytes_per_step": int(nrows * cols * 4),
                 "entry": "nlem_denoise_rows_host (C-ABI, pinned host buffers)"},
         "clocks": clk,
-        # per step: validate_image_kernel + pad_band_kernel + nlem_pixels_lr + nlem_pixels_tile over
-        # its hand-off list (profiles/r2_launches_bench.txt)
-        "gpu_launches": 4 * args.steps,
+        # per step: validate_image_kernel + pad_band_kernel + nlem_pixels_lr (small-mu probe and
+        # main launch) + nlem_pixels_tile over its hand-off list (profiles/r2_launches_bench.txt)
+        "gpu_launches": 5 * args.steps,
         "quality": {"psnr_noisy_db": psnr_noisy, "psnr_denoised_db": psnr_out},
         "secondary": secondary,
         "step_ms": [round(x, 2) for x in step_ms],

@@ -270,20 +270,15 @@ __global__ void __launch_bounds__(ALL, 1)
 admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
                 int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                 int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
-                int* ho_count, unsigned long long* invalid, int probe_n, int* probe_count) {
-  // probe_n > 0 (probe launch): probe_n problems spread evenly over the batch run up to the
-  // small-mu decision of sweep 1 and count predicted hand-offs into *probe_count; no outputs.
-  // probe_n == 0 with probe_count (main launch): when more than 90 % of the probed problems
-  // would be handed off (the small-mu regime), every problem is, right after its fused input
-  // validation - the exact p-form kernel then takes the whole batch (deterministic: the
-  // decision depends on the input only).
-  bool all_mode = false;
-  if (probe_n == 0 && probe_count != nullptr) {
-    const int64_t pt = batch < kProbe ? batch : kProbe;
-    all_mode = 10 * static_cast<int64_t>(*static_cast<volatile int*>(probe_count)) > 9 * pt;
-  }
-  const int64_t nidx = probe_n ? probe_n : batch;
-  auto prob_of = [&](int64_t i) { return probe_n ? i * batch / probe_n : i; };
+                int* ho_count, unsigned long long* invalid, const int* probe_count) {
+  // probe_count (optional): predicted small-mu hand-offs of kProbe sampled problems
+  // (small_mu_probe_kernel).  Above 90 % the whole batch is in the small-mu regime (lambda =
+  // w/mu >= ||p||: prox scales of 1, no decaying history, a ring overflow after R sweeps), and
+  // every problem goes to the exact kernel right after its fused input validation.  The
+  // decision depends on the input only (deterministic).
+  const int64_t pt = batch < kProbe ? batch : kProbe;
+  const bool all_mode =
+      probe_count != nullptr && 10 * static_cast<int64_t>(*static_cast<const volatile int*>(probe_count)) > 9 * pt;
   extern __shared__ __align__(16) float smem[];
   float* const stage = smem + SM_STAGE;
   float* const wst = smem + SM_WST;
@@ -315,15 +310,14 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #ifdef NLEM_BLR_STAMPS
   long long su_wait = 0, su_load = 0, su_pref = 0, su_init = 0, su_sw = 0, su_epi = 0, su_n = 0;
 #endif
-  int64_t b = prob_of(blockIdx.x);
-  if (static_cast<int64_t>(blockIdx.x) < nidx) {
+  int64_t b = blockIdx.x;
+  if (b < batch) {
     stage_copy(stage, points + b * nd, nd);
     stage_copy(wst, weights + b * n, n);
   }
   cp_commit();
 
-  for (int64_t ib = blockIdx.x; ib < nidx; ib += gridDim.x) {
-    b = prob_of(ib);
+  for (; b < batch; b += gridDim.x) {
 #ifdef NLEM_BLR_STAMPS
     const long long su_t0 = clock64();
 #endif
@@ -363,19 +357,15 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #ifdef NLEM_BLR_STAMPS
     const long long su_t2 = clock64(); su_load += su_t2 - su_t1;
 #endif
-    if (ib + gridDim.x < nidx) {
-      const int64_t bn = prob_of(ib + gridDim.x);
+    const int64_t bn = b + gridDim.x;
+    if (bn < batch) {
       stage_copy(stage, points + bn * nd, nd);
       stage_copy(wst, weights + bn * n, n);
     }
     cp_commit();
-    // exact stop possible (the p-form kernel decides it structurally), or the whole batch
-    // goes to the exact kernel (all_mode)
+    // exact stop possible (the p-form kernel decides it structurally), or the small-mu regime
     if (static_eq || all_mode) {
-      if (tid == 0) {
-        if (probe_n) atomicAdd(probe_count, 1);
-        else ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
-      }
+      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       continue;
     }
 
@@ -509,24 +499,16 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       }
       fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
       BLR_STAMP(s4);
-      // the sweep barrier also votes: a ring overflow, cancellation or non-finite value
-      // anywhere hands the problem to the exact kernel - stop sweeping now
-      const int stop = __syncthreads_or(bad || ovf);
+      __syncthreads();
       BLR_STAMP(s5);
-      if (t == 1 && T > R && 2 * __syncthreads_count(real_me && s == 1.0f) > n) ovf = true;
-      if (stop || ovf || probe_n) break;
 #ifdef NLEM_BLR_STAMPS
       st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
       st_q[0] += q0 - s1; st_q[1] += q1 - q0; st_q[2] += q2 - s3; st_q[3] += q3 - q2; st_q[4] += q4 - q3; st_q[5] += s4 - q4;
 #endif
      } else {
       BLR_STAMP(s4);
-      const int stop = __syncthreads_or(bad);
+      __syncthreads();
       BLR_STAMP(s5);
-      // small-mu regime (lambda = w/mu >= ||p||, e.g. the reference default mu = 1e-3): with most
-      // prox scales exactly 1 no history term decays and the ring overflows after R sweeps
-      if (t == 1 && T > R && 2 * __syncthreads_count(false) > n) ovf = true;
-      if (stop || ovf || probe_n) break;
 #ifdef NLEM_BLR_STAMPS
       st_b1 += s5 - s4;
 #endif
@@ -598,13 +580,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
-      if (tid == 0) {
-        if (probe_n) atomicAdd(probe_count, 1);
-        else ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
-      }
+      if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       continue;
     }
-    if (probe_n) continue;
     if (warp == CW) {
       if (cv0) z_out[b * D + cj] = z0;
       if (cv1) z_out[b * D + cj + 1] = z1;
@@ -878,26 +856,77 @@ bool admm_lr_supported(const AdmmLaunch& L) {
          static_cast<int64_t>(L.n) * D < (int64_t(1) << 31) / 4;
 }
 
+// Small-mu probe (one CTA per sampled problem, kProbe problems spread over the batch): at
+// sweep 1 the ADMM local copies start from p_k = z_0 - a_k, so point k's prox scale saturates
+// (s_k = 1) iff lambda_k = w_k / mu >= ||z_0 - a_k||.  A problem counts when more than half of
+// its points saturate (the test admm_batched_lr applied at sweep 1 in round 1).
+__global__ void __launch_bounds__(256)
+small_mu_probe_kernel(const float* __restrict__ points, const float* __restrict__ weights,
+                      int64_t batch, int n, const float* __restrict__ z_init, float mu, int pn,
+                      int* probe_count) {
+  __shared__ float z0[D];
+  __shared__ float part[8];
+  __shared__ int sat;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * batch / pn;
+  const float* a = points + b * n * D;
+  const float* w = weights + b * n;
+  if (threadIdx.x == 0) sat = 0;
+  // z_0: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
+  float ws = 0.0f;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) ws += w[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+  if (lane == 0) part[warp] = ws;
+  __syncthreads();
+  float W = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) W += part[i];
+  for (int j = threadIdx.x; j < D; j += blockDim.x) {
+    float m = 0.0f;
+    if (z_init != nullptr) {
+      m = z_init[b * D + j];
+    } else {
+      for (int k = 0; k < n; ++k) m = fmaf(a[static_cast<int64_t>(k) * D + j], w[k] / W, m);
+    }
+    z0[j] = m;
+  }
+  __syncthreads();
+  int cnt = 0;
+  for (int k = warp; k < n; k += 8) {
+    float s2 = 0.0f;
+    for (int j = lane; j < D; j += 32) {
+      const float e = z0[j] - a[static_cast<int64_t>(k) * D + j];
+      s2 = fmaf(e, e, s2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const float lam = w[k] / mu;
+    cnt += lam * lam >= s2 && lam > 0.0f;
+  }
+  if (lane == 0) atomicAdd(&sat, cnt);
+  __syncthreads();
+  if (threadIdx.x == 0 && 2 * sat > n) atomicAdd(probe_count, 1);
+}
+
 cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int* probe,
                            cudaStream_t stream) {
   auto kfn = admm_batched_lr;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  const int sms = device_caps().sms;
-  if (probe != nullptr && L.max_iter > R) {  // small-mu probe (probe[0] = predicted hand-offs)
+  if (probe != nullptr && L.max_iter > R) {
     const int pn = static_cast<int>(std::min<int64_t>(L.batch, kProbe));
-    kfn<<<static_cast<unsigned>(std::min(pn, sms)), ALL, SMEM_BYTES, stream>>>(
-        L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
-        L.iters_out, ho_list, ho_count, L.invalid, pn, probe);
+    small_mu_probe_kernel<<<pn, 256, 0, stream>>>(L.points, L.weights, L.batch, L.n, L.z_init,
+                                                  L.mu, pn, probe);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   } else {
     probe = nullptr;
   }
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, sms));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
-      L.iters_out, ho_list, ho_count, L.invalid, 0, probe);
+      L.iters_out, ho_list, ho_count, L.invalid, probe);
   return cudaGetLastError();
 }
 

@@ -3,6 +3,7 @@
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
+#include <utility>
 
 #include "nlem_b200.hpp"
 
@@ -111,6 +112,34 @@ int main() {
     for (int r = 0; r < 23; ++r)
       for (int c = 0; c < 17; ++c) same &= one(r, c) == three(r, c);
     CHECK(same);
+  }
+  {  // solve_patch on a build_patch_stack stack (nlem.hpp:60-62, patch.cpp:90-114): the centre
+     // coordinate of the solved patch is the pixel nlem_denoise writes (nlem.cpp:84)
+    Image img(15, 13);
+    for (int r = 0; r < 15; ++r)
+      for (int c = 0; c < 13; ++c) img(r, c) = static_cast<float>((r * 53 + c * 29) % 200);
+    NlemParams p = params;
+    p.mu = 1.0;
+    Image out = nlem_denoise(img, p);
+    for (const auto& rc : {std::pair<int, int>{0, 0}, std::pair<int, int>{7, 6}, std::pair<int, int>{14, 12}}) {
+      PatchStack st = build_patch_stack(img, rc.first, rc.second, p.search, p.patch, p.h);
+      CHECK(st.d == 9 && st.weights[st.self_column] == 1.0f);
+      PatchSolve s = solve_patch(st, p);
+      std::vector<float> init = initial_patch(st, PatchInit::NoisyPatch);
+      bool self = true;
+      for (int j = 0; j < 9; ++j) self &= init[j] == st.patches[st.self_column * 9 + j] && s.init[j] == init[j];
+      CHECK(self);
+      CHECK(std::fabs(s.patch[4] - out(rc.first, rc.second)) <= 1e-2f);
+    }
+    PatchStack bad = build_patch_stack(img, 3, 3, 3, 3, 10.0);
+    bad.self_column = 99;
+    bool threw = false;
+    try {
+      solve_patch(bad, p);
+    } catch (const std::invalid_argument& e) {
+      threw = std::string(e.what()).find("self column") != std::string::npos;
+    }
+    CHECK(threw);
   }
   CHECK(default_init_mode(60.5) == PatchInit::NlmPatch);
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "OK", failures);

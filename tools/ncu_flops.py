@@ -40,6 +40,7 @@ for rec in csv.reader(io.StringIO(txt)):
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 d = dict(zip(rows[0], rows[2])) if len(rows) > 2 else {}
+units = dict(zip(rows[0], rows[1])) if len(rows) > 1 else {}
 
 
 def num(k):
@@ -49,7 +50,8 @@ def num(k):
         return float("nan")
 
 
-dur_ns = num("gpu__time_duration.sum")
+_scale = {"nsecond": 1.0, "ns": 1.0, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6, "second": 1e9, "s": 1e9}
+dur_ns = num("gpu__time_duration.sum") * _scale.get(units.get("gpu__time_duration.sum", "nsecond"), 1.0)
 flops = sum(ops[k] * 32 * f for k, f in FLOPS.items())
 res = {
     "kernel": d.get("Kernel Name", "")[:160],
@@ -62,7 +64,6 @@ res = {
     "smem_wavefronts_pct": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
     "smem_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
     "dram_bytes": num("dram__bytes_read.sum") + num("dram__bytes_write.sum"),
-    "sm_mhz_under_ncu": num("sm__cycles_elapsed.avg.per_second") / 1e6,
     "note": "flops = executed warp instructions x 32 x flops per opcode (upper bound: inactive "
             "lanes of a partially predicated instruction are counted)",
 }
