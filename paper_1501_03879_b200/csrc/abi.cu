@@ -398,7 +398,11 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
                cfg.mu, cfg.max_iter, cfg.tol_primal,
                res_mode_for(cfg.tol_primal, trace_residual != nullptr), z_out, objective_out,
                iters_out, trace_objective, trace_residual, nullptr};
-  const bool lr = admm_lr_supported(L);
+  // NLEM_BATCHED_KERNEL=fast|generic forces a kernel family (A/B measurements, tests; read per
+  // call); the default is the best specialised kernel for the shape
+  const char* force = std::getenv("NLEM_BATCHED_KERNEL");
+  const std::string fk = force ? force : "";
+  const bool lr = fk.empty() && admm_lr_supported(L);
   // validation: fused into the low-rank kernel (no extra pass over the points), else separate
   DevSlot inval(s);
   if (failure && lr) {
@@ -434,7 +438,7 @@ nlem_status nlem_admm_batched(const float* points, const float* weights, int64_t
       if (e == cudaSuccess) e = ef;
     }
   } else {
-    e = admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
+    e = fk != "generic" && admm_fast_supported(L) ? launch_admm_fast(L, s) : launch_admm_generic(L, s);
   }
   // Collinear point sets (affine rank 1) are one-dimensional problems: with tol 0 their exact
   // residual stop is reachable (as for d <= 16) and only the reference-form sweep reproduces

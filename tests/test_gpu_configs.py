@@ -102,3 +102,40 @@ def test_config4_sweep_vs_oracle(nb, oracle, sigma):
         assert err.max() <= TOL, (solver, err.max(), np.unravel_index(err.argmax(), err.shape))
         for t in range(100):
             assert abs(_psnr(fg[t], c) - _psnr(fo[t], c)) <= PSNR_TOL, (solver, t)
+
+
+@pytest.mark.parametrize("cfg,k,S", [(0, 5, 11), (2, 7, 21)])
+@pytest.mark.parametrize("iters", [10, 30])
+def test_irls_tol0_loose(nb, oracle, cfg, k, S, iters):
+    """NLEM-IRLS with the reference's own stop rule, tol = 0 (nlem.cpp:45-48, irls.hpp:58: stop
+    on the first non-decrease of the surrogate).  The FP32 surrogate stalls a few passes before
+    the FP64 one (measured: ~3 passes earlier on average), so the bar is loose:
+    the stop pass per pixel (read from the forward-filled frames) within 25 passes, max |d| <=
+    0.1 and the 99th percentile <= 0.05 gray levels, |dPSNR| <= 0.01 dB - against the tight
+    1e-2 bar of the fixed-count (tol < 0) runs in test_config4_sweep_vs_oracle."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(cfg)
+    if cfg == 2:
+        clean, noisy = clean[:96, :128], noisy[:96, :128]
+    h = synth.reference_h(20.0, k * k)
+    g = nb.NlemParams(search=S, patch=k, h=h, sigma=20.0, solver="irls", solver_iters=iters,
+                      epsilon=1e-6, irls_tol=0.0)
+    o = oracle.make_params(search=S, patch=k, h=h, sigma=20.0, solver="irls", solver_iters=iters,
+                           epsilon=1e-6, irls_tol=0.0)
+    fg = nb.nlem_denoise_snapshots(noisy, g).astype(np.float64)
+    _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
+
+    def stop_pass(f):
+        same = np.ones(f.shape[1:], bool)
+        st = np.full(f.shape[1:], f.shape[0])
+        for t in range(f.shape[0] - 1, 0, -1):
+            same &= f[t] == f[t - 1]
+            st[same] = t
+        return st
+
+    assert np.abs(stop_pass(fg) - stop_pass(fo)).max() <= 25
+    d = np.abs(fg[-1] - fo[-1])
+    assert d.max() <= 0.1 and np.percentile(d, 99) <= 0.05, (d.max(), np.percentile(d, 99))
+    c = clean.astype(np.float64)
+    assert abs(_psnr(fg[-1], c) - _psnr(fo[-1], c)) <= PSNR_TOL

@@ -52,3 +52,4 @@ for mu in (1.0, 1e-3):
         ts.append(a.elapsed_time(b))
     t = min(ts[1:])
     print(f"config1 mu={mu} B={B}: {t:.2f} ms = {B / t / 1e3:.3f} M problems/s", flush=True)
+print(f"(NLEM_BATCHED_KERNEL={os.environ.get('NLEM_BATCHED_KERNEL', 'default')})")
