@@ -95,3 +95,19 @@ def test_point_set_generator():
     inl = p[:, :397]
     assert 40 < inl.mean() < 210
     assert p[:, 397:].min() >= 0 and p[:, 397:].max() <= 255
+
+
+def test_host_entry_rejects_bad_out_buffers():
+    """A caller-supplied host `out` must be a writeable C-contiguous float32 array of the
+    output shape (the C ABI writes rows*cols floats through its pointer) - checked before
+    any device work."""
+    p = api.NlemParams(search=7, patch=3, h=30.0, solver_iters=2)
+    img = np.zeros((6, 5), np.float32)
+    for bad in (np.zeros((6, 5), np.float64), np.zeros((5, 6), np.float32),
+                np.zeros((6, 10), np.float32)[:, ::2], np.zeros(30, np.float32)):
+        with pytest.raises(api.InvalidArgument, match="out must be"):
+            api.nlem_denoise_host(img, p, out=bad)
+    with pytest.raises(api.InvalidArgument, match="out must be"):
+        api.nlem_denoise_rows_host(img, 0, 6, 5, 0, 3, p, out=np.zeros((6, 5), np.float32))
+    with pytest.raises(api.InvalidArgument, match=r"\[in_rows\]\[cols\]"):
+        api.nlem_denoise_rows_host(img[:, :4], 0, 6, 5, 0, 3, p)
