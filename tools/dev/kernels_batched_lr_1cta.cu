@@ -1,5 +1,5 @@
 // Low-rank (Gram-form) EM-ADMM for batched standalone solves, d = 49, 3 <= n <= 448
-// (BASELINE config 1: 65,536 problems x n = 441 x d = 49), and the batched IRLS comparator.
+// (BASELINE config 1: 65,536 problems x n = 441 x d = 49).
 //
 // Algebra: the p-form of admm.hpp:49-78 unrolled as in kernels_nlem_lr.cu.  With everything
 // centred on m = z_0 (the initial consensus: the weighted mean, admm.hpp:40, or z_init),
@@ -17,56 +17,41 @@
 // non-finite value is handed, through a device-side list, to the exact p-form kernel
 // (admm_batched_fast), which then owns its outputs and failure record.
 //
-// Mapping (B200), round 2: TWO problems in flight per SM.  A sweep is a serial chain (dot
-// products -> group reduction -> per-point scalar update -> weighted sum -> CTA reduction ->
-// consensus -> next dot products); with one problem per SM (round 1: 14 point warps at 128
-// registers, every warp in the same phase) the FMA pipe sat idle for most of the chain.  Now one
-// problem is a CTA of 7 point warps + 1 consensus warp at 128 registers and two CTAs share an
-// SM, so one problem's reductions and barriers overlap the other's FFMA2s, and one problem's
-// setup (load, validation, weighted mean, centring) overlaps the other's sweeps.
-//  * groups of 8 lanes own 16 points as 8 float2 point pairs, each lane 7 contiguous
-//    coordinates (j = 7 g + i, d padded to 56), so both passes are FFMA2 on a point pair;
-//    pairs 0..3 of a group live in REGISTERS (56 per lane), pairs 4..7 in TENSOR MEMORY (56
-//    columns of the lane, one tcgen05.ld pass of 16 + 16 + 16 + 8 columns per MAC pass) - the
-//    register file holds one problem per SM, so the second problem's worth of points sits in
-//    TMEM, whose read path (~176 B/clk/SM measured, tools/tmem_bw.cu) is separate from the
-//    shared-memory / shuffle data pipe that the reductions already load (a shared-memory
-//    resident half measured that pipe at 68 % with no gain over one problem per SM);
-//  * lane g of a group owns the scalar state of point slots g and 8 + g: reduce-scatter of the
-//    dot products in the group, scalar updates, all-gather of ga';
+// Mapping (B200): one problem per CTA of 14 point warps + 1 consensus warp, 1 CTA per SM.
+//  * the centred points live in REGISTERS (the p-form kernel kept them in shared memory and
+//    re-read them every sweep): groups of 8 lanes own 8 points, each lane 7 contiguous
+//    coordinates (j = 7 g + i, d padded to 56) as float2 point pairs, so both passes are FFMA2;
+//  * lane g of a group owns the scalar state of point slot g: reduce-scatter of the 8 dot
+//    products in the group, scalar update, all-gather of ga';
 //  * each point warp folds its 4 groups and writes one 64-column partial row (coordinates at
 //    columns 8 g + i, history sums sum_k al'_r in columns 8 r + 7); after the CTA barrier the
-//    consensus warp sums the 7 rows in a fixed tree, forms z_t and c~_{t+1}, publishes c~
+//    consensus warp sums the 14 rows in a fixed tree, forms z_t and c~_{t+1}, publishes c~
 //    (named barrier 1) and then the Gram row (named barrier 2), so the point warps' dot products
 //    overlap the Gram reduction; ptxas moves arithmetic across bar.sync, so the order is pinned
 //    with a shared-memory store before each wait and a reload after the arrive;
-//  * points are read straight from HBM / L2 at the start of a problem (the next problem's lines
-//    are prefetched into L2 during the sweeps); the co-resident CTA hides the latency.
+//  * the next problem's points and weights stream into a shared-memory staging buffer with
+//    16-byte cp.async during the current problem's sweeps.
 // The batched IRLS kernel (irls_batched_reg, below) reuses the layout and the consensus warp.
 #include <algorithm>
 #include <cstdint>
-#include <cstdio>
 #include <cstdlib>
 #include <string>
+#ifdef NLEM_BLR_STAMPS
+#include <cstdio>
+#endif
 
 #include "launch.h"
-#include "tmem.cuh"
 
 namespace nlemk {
 
 namespace blr {
 
-constexpr int D = 49, G = 8, J = 7;
-constexpr int KR = 4, KS = 4, KP = KR + KS;  // float2 point pairs per group: registers, smem
-constexpr int WARPS = 7;                     // point warps
-constexpr int CW = WARPS;                    // the consensus warp (no points)
+constexpr int D = 49, G = 8, J = 7, KP = G / 2;
+constexpr int WARPS = 14;          // point warps
+constexpr int CW = WARPS;          // the consensus warp (no points)
 constexpr int NW = WARPS + 1, ALL = 32 * NW;
-constexpr int PT = 32 * WARPS;               // point threads
-constexpr int GPW = 32 / G, NG = GPW * WARPS, NCAP = NG * 2 * KP;  // 28 groups, 448 points
+constexpr int GPW = 32 / G, NG = GPW * WARPS, NCAP = NG * G;  // 56 groups, 448 points
 constexpr int R = 4;
-constexpr int TM_HALF = KS * J * 2;          // TMEM columns per lane: the second half of its points
-constexpr int TM_WCOLS = 64;                 // column slice of one warp (warps w and w + 4 share lanes)
-constexpr int TM_COLS = 128;                 // TMEM columns allocated per CTA
 // Column layout of every per-coordinate row (partials, c~, m): lane g of a group owns
 // coordinates j = 7 g + i (i < 7) at columns 8 g + i; column 8 g + 7 carries the history sum
 // sum_k al'_g for g < 4 (partial rows) and is 0 otherwise.
@@ -75,7 +60,9 @@ constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2: ring term below
 constexpr float kCancel = 1.0f / 256.0f;           // N below 2^-8 (H + ||c~||^2): cancellation
 constexpr int kProbe = 64;                         // problems sampled by the small-mu probe
 // shared memory (floats)
-constexpr int SM_RED = 0;                        // [WARPS][RS] per-warp partial rows
+constexpr int SM_STAGE = 0;                      // raw points of the next problem (+4 shift)
+constexpr int SM_WST = SM_STAGE + NCAP * D + 4;  // raw weights of the next problem (+4 shift)
+constexpr int SM_RED = SM_WST + NCAP + 4;        // [WARPS][RS] per-warp partial rows
 // Published rows (c~ / x, m) are read by every point lane as two 16-byte loads at column 8 g:
 // columns 32..63 sit 4 floats further on (RSK = RS + 4), so lanes g and g + 4 hit distinct banks
 // (one wavefront per load instead of two; these loads follow the row barrier on every warp).
@@ -85,23 +72,29 @@ constexpr int SM_MB = SM_CB + RSK;               // [RSK] m (centring), then z~ 
 constexpr int SM_GR = SM_MB + RSK;               // [8] Gram row: G_0..G_3, ||c~||^2, ||c~_{t-4}||^2
 constexpr int SM_SCAL = SM_GR + 8;               // [32] block-sum scratch
 constexpr int SM_PIN = SM_SCAL + 32;             // [ALL] barrier-ordering scratch
-constexpr int SM_TB = SM_PIN + ALL;               // [4] TMEM base address of the CTA
-constexpr int SM_TOTAL = SM_TB + 4;
+constexpr int SM_TOTAL = SM_PIN + ALL;
 constexpr size_t SMEM_BYTES = size_t(SM_TOTAL) * sizeof(float);
 static_assert(NCAP >= 441, "config-1 capacity");
-static_assert(TM_HALF == 56 && TM_HALF <= TM_WCOLS && 2 * TM_WCOLS <= TM_COLS, "TMEM layout");
-static_assert(SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_MB % 4 == 0 && SM_GR % 4 == 0, "alignment");
-static_assert(2 * (SMEM_BYTES + 1024) <= 233472, "two CTAs per SM");
+static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_MB % 4 == 0 &&
+              SM_GR % 4 == 0, "alignment");
 
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void cp16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 __device__ __forceinline__ float rsq(float x) {
   float y;
   asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 // named barriers: the consensus warp arrives, the other warps wait (count = all threads)
 __device__ __forceinline__ void bar_sync(int id) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(ALL) : "memory");
@@ -113,83 +106,41 @@ __device__ __forceinline__ void bar_arrive(int id) {
 // across them.  To keep work on the intended side, a value is stored to / reloaded from shared
 // memory at the barrier (a store cannot sink below it, a load cannot rise above it).
 constexpr int BAR_C = 1, BAR_GRAM = 2;
+#ifdef NLEM_BLR_STAMPS
+#define BLR_STAMP(v) long long v = clock64()
+#else
+#define BLR_STAMP(v)
+#endif
 
-// The TMEM-resident half of a lane's points: 56 columns holding the float2 point pairs of the
-// sequence e = 0..27 (pair m = KR + e / 7, coordinate i = e % 7) at columns 2e, 2e + 1, moved as
-// three 16-column accesses and one of 8.  f(m, i, v) sees compile-time m and i after unrolling.
-template <int E0, int NE, class F>
-__device__ __forceinline__ void tm_elems(const float* v, F&& f) {
-#pragma unroll
-  for (int q = 0; q < NE; ++q)
-    f(KR + (E0 + q) / J, (E0 + q) % J, make_float2(v[2 * q], v[2 * q + 1]));
+// element e of `src` lands at dst[shift(src) + e], shift = (src / 4) mod 4, so that global and
+// shared addresses agree mod 16 and the interior moves as 16-byte cp.async
+__device__ __forceinline__ int stage_shift(const float* src) {
+  return static_cast<int>((reinterpret_cast<uintptr_t>(src) >> 2) & 3);
 }
-template <class F>
-__device__ __forceinline__ void for_tm_half(uint32_t tp, F&& f) {
-  float v[16];
-  tm::ld16_wait<0>(tp, v);
-  tm_elems<0, 8>(v, f);
-  tm::ld16_wait<16>(tp, v);
-  tm_elems<8, 8>(v, f);
-  tm::ld16_wait<32>(tp, v);
-  tm_elems<16, 8>(v, f);
-  tm::ld8_wait<48>(tp, v);
-  tm_elems<24, 4>(v, f);
-}
-// gen(m, i) -> float2 written to the lane's TMEM half (no wait: the caller waits for the stores)
-template <int E0, int NE, class Gen>
-__device__ __forceinline__ void tm_fill(float* v, Gen&& gen) {
+__device__ __forceinline__ void stage_copy(float* dst, const float* src, int total) {
+  const int s0 = stage_shift(src);
+  const int nch = (s0 + total + 3) >> 2;
+  const float* base = src - s0;  // 16-byte aligned
+  for (int c = threadIdx.x; c < nch; c += ALL) {
+    const int e0 = 4 * c - s0;
+    if (e0 >= 0 && e0 + 3 < total) {
+      cp16(dst + 4 * c, base + 4 * c);
+    } else {
 #pragma unroll
-  for (int q = 0; q < NE; ++q) {
-    const float2 a = gen(KR + (E0 + q) / J, (E0 + q) % J);
-    v[2 * q] = a.x;
-    v[2 * q + 1] = a.y;
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q;
+        if (e >= 0 && e < total) cp4(dst + 4 * c + q, base + 4 * c + q);
+      }
+    }
   }
-}
-template <class Gen>
-__device__ __forceinline__ void store_tm_half(uint32_t tp, Gen&& gen) {
-  float v[16];
-  tm_fill<0, 8>(v, gen);
-  tm::st16<0>(tp, v);
-  tm_fill<8, 8>(v, gen);
-  tm::st16<16>(tp, v);
-  tm_fill<16, 8>(v, gen);
-  tm::st16<32>(tp, v);
-  tm_fill<24, 4>(v, gen);
-  tm::st8<48>(tp, v);
-}
-// f(m, i, old) -> new value, in place
-template <int E0, int NE, class F>
-__device__ __forceinline__ void tm_map_elems(float* v, F&& f) {
-#pragma unroll
-  for (int q = 0; q < NE; ++q) {
-    const float2 a = f(KR + (E0 + q) / J, (E0 + q) % J, make_float2(v[2 * q], v[2 * q + 1]));
-    v[2 * q] = a.x;
-    v[2 * q + 1] = a.y;
-  }
-}
-template <class F>
-__device__ __forceinline__ void map_tm_half(uint32_t tp, F&& f) {
-  float v[16];
-  tm::ld16_wait<0>(tp, v);
-  tm_map_elems<0, 8>(v, f);
-  tm::st16<0>(tp, v);
-  tm::ld16_wait<16>(tp, v);
-  tm_map_elems<8, 8>(v, f);
-  tm::st16<16>(tp, v);
-  tm::ld16_wait<32>(tp, v);
-  tm_map_elems<16, 8>(v, f);
-  tm::st16<32>(tp, v);
-  tm::ld8_wait<48>(tp, v);
-  tm_map_elems<24, 4>(v, f);
-  tm::st8<48>(tp, v);
 }
 
 // Reduce-scatter of 8 per-point values (4 float2 slots) across the 8 lanes of a group: lane g
 // returns the sum for point slot g.  Fixed tree (bitwise deterministic).
-__device__ __forceinline__ float group_rs8(const float2* v, int g) {
+__device__ __forceinline__ float group_rs8(const float2 (&v)[KP], int g) {
   float x[G];
 #pragma unroll
-  for (int m = 0; m < G / 2; ++m) {
+  for (int m = 0; m < KP; ++m) {
     x[2 * m] = v[m].x;
     x[2 * m + 1] = v[m].y;
   }
@@ -206,10 +157,10 @@ __device__ __forceinline__ float group_rs8(const float2* v, int g) {
   return x[0];
 }
 // All-gather of one value per lane of the group into 4 float2 slots (slot 2m, 2m+1).
-__device__ __forceinline__ void group_ag8(float mine, float2* out, int lane) {
+__device__ __forceinline__ void group_ag8(float mine, float2 (&out)[KP], int lane) {
   const int base = lane & ~(G - 1);
 #pragma unroll
-  for (int m = 0; m < G / 2; ++m) {
+  for (int m = 0; m < KP; ++m) {
     out[m].x = __shfl_sync(0xffffffffu, mine, base + 2 * m);
     out[m].y = __shfl_sync(0xffffffffu, mine, base + 2 * m + 1);
   }
@@ -240,7 +191,7 @@ __device__ __forceinline__ float2 rows_sum(const float* red, int lane) {
   return r[0];
 }
 // columns 2 l, 2 l + 1 of a published row: the consensus lane l's pair.  SKEW (ADMM): columns
-// 32..63 4 floats on; the IRLS kernel keeps the plain row.
+// 32..63 4 floats on; the IRLS kernel measured 1.5 % slower with the skew and keeps the plain row.
 template <bool SKEW = true>
 __device__ __forceinline__ float2* pub_pair(float* row, int lane) {
   return reinterpret_cast<float2*>(row + 2 * lane + (SKEW ? ((lane >> 4) << 2) : 0));
@@ -255,7 +206,7 @@ __device__ __forceinline__ void load_coords(const float* row, int g, float (&c)[
   c[4] = b.x; c[5] = b.y; c[6] = b.z;
 }
 // Block sum of one value per thread (fixed order), valid in thread 0 only.  One barrier: the
-// next write of `scal` happens after the next problem's barriers.
+// next write of `scal` happens after the next problem's top-of-loop barrier.
 __device__ __forceinline__ float block_sum0(float v, float* scal, int warp, int lane) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -268,56 +219,18 @@ __device__ __forceinline__ float block_sum0(float v, float* scal, int warp, int 
   return t;
 }
 
-// One problem's points and weights from global memory: pairs 0..KR-1 into registers, pairs KR..
-// into this lane's TMEM columns (raw), with the fused input validation (types.hpp:58-68, the
-// checks validate_points_dev runs as a separate pass) and the all-points-equal test.  Padding
-// slots (k >= n, coordinates >= 49) hold finite 0.  Returns (any element != point 0's).
-struct Loaded {
-  bool bad_pt, neq;
-};
-__device__ __forceinline__ Loaded load_problem(const float* __restrict__ src,
-                                               const float* __restrict__ wsrc, int n, int gid,
-                                               int g, bool is_pts, float2 (&A)[KR][J],
-                                               float2 (&wq)[KP], uint32_t tp) {
-  const bool greal = is_pts && g < 7;  // lane g = 7 of a group: padding coordinates 49..55
-  const float* const col = src + 7 * g;
-  float r0[J];
-#pragma unroll
-  for (int i = 0; i < J; ++i) r0[i] = greal ? __ldg(col + i) : 0.0f;
-  bool bad = false, neq = false;
-  auto fetch = [&](int m, int i) {
-    const int k0 = 2 * (m * NG + gid);
-    const bool h0 = greal && k0 < n, h1 = greal && k0 + 1 < n;
-    const float v0 = h0 ? __ldg(col + k0 * D + i) : r0[i];
-    const float v1 = h1 ? __ldg(col + (k0 + 1) * D + i) : r0[i];
-    neq |= (v0 != r0[i]) | (v1 != r0[i]);
-    bad |= !isfinite(v0) | !isfinite(v1);
-    return make_float2(h0 ? v0 : 0.0f, h1 ? v1 : 0.0f);
-  };
-  if (is_pts) {
-    store_tm_half(tp, fetch);
-    tm::wait_st();
-  }
-#pragma unroll
-  for (int m = 0; m < KR; ++m)
-#pragma unroll
-    for (int i = 0; i < J; ++i) A[m][i] = fetch(m, i);
-#pragma unroll
-  for (int m = 0; m < KP; ++m) {
-    const int k0 = 2 * (m * NG + gid);
-    wq[m] = make_float2(is_pts && k0 < n ? __ldg(wsrc + k0) : 0.0f,
-                        is_pts && k0 + 1 < n ? __ldg(wsrc + k0 + 1) : 0.0f);
-  }
-  return Loaded{bad, neq};
-}
-// lowest failing (problem << 2 | code) wins; code 1 coordinates, 2 weights, 3 no positive
-// weight - the reference's order within a problem.  One barrier per problem.
-__device__ __forceinline__ void check_problem(bool bad_pt, const float2 (&wq)[KP], int64_t b,
-                                              unsigned long long* invalid) {
+// Fused input validation (types.hpp:58-68, the checks validate_points_dev runs as a separate
+// pass): every thread checks the coordinates and weights it loaded (padding slots hold finite 0),
+// the lowest failing (problem << 2 | code) wins; code 1 coordinates, 2 weights, 3 no positive
+// weight - the reference's order within a problem.  One extra barrier per problem.
+__device__ __forceinline__ void check_problem(const float2 (&A)[KP][J], const float2 (&wq)[KP],
+                                              int64_t b, unsigned long long* invalid) {
   if (invalid == nullptr) return;  // uniform
-  bool bad_w = false, pos = false;
+  bool bad_pt = false, bad_w = false, pos = false;
 #pragma unroll
   for (int m = 0; m < KP; ++m) {
+#pragma unroll
+    for (int i = 0; i < J; ++i) bad_pt |= !isfinite(A[m][i].x) || !isfinite(A[m][i].y);
     bad_w |= !(isfinite(wq[m].x) && wq[m].x >= 0.0f) || !(isfinite(wq[m].y) && wq[m].y >= 0.0f);
     pos |= wq[m].x > 0.0f || wq[m].y > 0.0f;
   }
@@ -326,59 +239,34 @@ __device__ __forceinline__ void check_problem(bool bad_pt, const float2 (&wq)[KP
   if (bad_w) atomicMin(invalid, key | 2ull);
   if (!__syncthreads_or(pos) && threadIdx.x == 0) atomicMin(invalid, key | 3ull);
 }
-// the lines of one problem into L2 (128-byte steps over points and weights)
-__device__ __forceinline__ void prefetch_problem(const float* src, const float* wsrc, int nd,
-                                                 int n) {
-  const char* p = reinterpret_cast<const char*>(src);
-  for (int o = threadIdx.x * 128; o < nd * 4; o += ALL * 128) prefetch_l2(p + o);
-  const char* w = reinterpret_cast<const char*>(wsrc);
-  for (int o = threadIdx.x * 128; o < n * 4; o += ALL * 128) prefetch_l2(w + o);
-}
 
 // Weighted-mean numerator and denominator in one row pass (admm.hpp:40 / irls.hpp:32 with
 // types.hpp:71-74): the point warps write sum_k w_k a_k per coordinate and the weight sum (column
 // 7) into their partial rows; one barrier; the consensus warp divides (sum w a) / (sum w).
-__device__ __forceinline__ void weighted_sum_rows(const float2 (&A)[KR][J], uint32_t tp,
-                                                  const float2 (&wq)[KP], float* myrow,
-                                                  bool is_pts, int lane) {
-  if (is_pts) {
-    float2 acc[J];
+__device__ __forceinline__ void weighted_sum_rows(const float2 (&A)[KP][J], const float2 (&wq)[KP],
+                                                  float* myrow, bool is_pts, int lane) {
+  float v[J];
 #pragma unroll
-    for (int i = 0; i < J; ++i) acc[i] = make_float2(0.0f, 0.0f);
+  for (int i = 0; i < J; ++i) {
+    float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-    for (int m = 0; m < KR; ++m)
-#pragma unroll
-      for (int i = 0; i < J; ++i) acc[i] = __ffma2_rn(wq[m], A[m][i], acc[i]);
-    for_tm_half(tp, [&](int m, int i, float2 a) { acc[i] = __ffma2_rn(wq[m], a, acc[i]); });
-    float v[J];
-#pragma unroll
-    for (int i = 0; i < J; ++i) v[i] = acc[i].x + acc[i].y;
-    float ws = 0.0f;  // weights of this lane's group (same in its 8 lanes), then of the warp
-#pragma unroll
-    for (int m = 0; m < KP; ++m) ws += wq[m].x + wq[m].y;
-    ws += __shfl_xor_sync(0xffffffffu, ws, 8);
-    ws += __shfl_xor_sync(0xffffffffu, ws, 16);
-    fold_store(v, lane == 0 ? ws : 0.0f, myrow, lane);
+    for (int m = 0; m < KP; ++m) acc = __ffma2_rn(wq[m], A[m][i], acc);
+    v[i] = acc.x + acc.y;
   }
-  __syncthreads();
-}
-
-// warp sums of four per-lane values (x0..x3) onto lanes r = lane & 3 (value x_r)
-__device__ __forceinline__ float quad_sums(float x0, float x1, float x2, float x3, int lane) {
-  const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
-  const float y0 = (u2 ? x2 : x0) + __shfl_xor_sync(0xffffffffu, u2 ? x0 : x2, 2);
-  const float y1 = (u2 ? x3 : x1) + __shfl_xor_sync(0xffffffffu, u2 ? x1 : x3, 2);
-  float hs = (u1 ? y1 : y0) + __shfl_xor_sync(0xffffffffu, u1 ? y0 : y1, 1);
+  float ws = 0.0f;  // weights of this lane's group (same in its 8 lanes), then of the warp
 #pragma unroll
-  for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
-  return hs;
+  for (int m = 0; m < KP; ++m) ws += wq[m].x + wq[m].y;
+  ws += __shfl_xor_sync(0xffffffffu, ws, 8);
+  ws += __shfl_xor_sync(0xffffffffu, ws, 16);
+  if (is_pts) fold_store(v, lane == 0 ? ws : 0.0f, myrow, lane);
+  __syncthreads();
 }
 
 }  // namespace blr
 
 using namespace blr;
 
-__global__ void __launch_bounds__(ALL, 2)
+__global__ void __launch_bounds__(ALL, 1)
 admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weights,
                 int64_t batch, int n, const float* __restrict__ z_init, nlem_box box, float mu,
                 int T, float* z_out, float* obj_out, int* iters_out, int* ho_list,
@@ -392,6 +280,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const bool all_mode =
       probe_count != nullptr && 10 * static_cast<int64_t>(*static_cast<const volatile int*>(probe_count)) > 9 * pt;
   extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
   float* const red = smem + SM_RED;
   float* const cb = smem + SM_CB;
   float* const mb = smem + SM_MB;
@@ -404,19 +294,11 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const int g = lane & (G - 1);
   const int gid = warp * GPW + (lane >> 3);
   const bool is_pts = warp < WARPS;
-  // TMEM: the second half of every lane's points (128 columns per CTA, two CTAs per SM)
-  const uint32_t tbase = tm::alloc_cta<TM_COLS>(reinterpret_cast<uint32_t*>(smem + SM_TB), warp);
-  const uint32_t tp = tm::warp_addr(tbase, warp, (warp >> 2) * TM_WCOLS);
   float* const myrow = red + (is_pts ? warp : 0) * RS;
-  const bool greal = is_pts && g < 7;
-  // this lane's two point slots: slot h is side g & 1 of pair KR h + g / 2
-  int k_me[2];
-  bool real_me[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    k_me[h] = 2 * ((KR * h + (g >> 1)) * NG + gid) + (g & 1);
-    real_me[h] = is_pts && k_me[h] < n;
-  }
+  // point of slot q of this lane's group: pair m = q / 2 is point pair m * NG + gid
+  auto point_of = [&](int q) { return 2 * ((q >> 1) * NG + gid) + (q & 1); };
+  const int k_me = point_of(g);
+  const bool real_me = is_pts && k_me < n;
   // consensus (warp CW): lane l finishes columns 2l, 2l+1 = coordinates cj, cj + 1
   const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
   const int cj = 7 * cgrp + cidx;
@@ -425,30 +307,74 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const float inv_n = 1.0f / static_cast<float>(n);
   const int nd = n * D;
 
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    // ---- this problem's points (raw) into registers / smem, weights, all-equal test
+#ifdef NLEM_BLR_STAMPS
+  long long su_wait = 0, su_load = 0, su_pref = 0, su_init = 0, su_sw = 0, su_epi = 0, su_n = 0;
+#endif
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+
+  for (; b < batch; b += gridDim.x) {
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t0 = clock64();
+#endif
+    cp_wait_all();
+    __syncthreads();
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t1 = clock64(); su_wait += su_t1 - su_t0;
+#endif
+    // ---- this problem's points (raw) into registers, weights, all-equal test
     const float* const src = points + b * nd;
-    const float* const wsrc = weights + b * n;
-    float2 A[KR][J];
+    const float* const st = stage + stage_shift(src);
+    const float* const wv = wst + stage_shift(weights + b * n);
+    float2 A[KP][J];
     float2 wq[KP];
-    const Loaded ld = load_problem(src, wsrc, n, gid, g, is_pts, A, wq, tp);
-    float w_me[2];
+    int neq = 0;
+    const bool greal = is_pts && g < 7;  // lane g = 7 of a group: padding coordinates 49..55
+    float r0[J];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? __ldg(wsrc + k_me[h]) : 0.0f;
-    check_problem(ld.bad_pt, wq, b, invalid);
-    // every warp is past the previous problem (its pin / scal / mb reads) after this barrier
-    const bool static_eq = !__syncthreads_or(ld.neq);
-    if (b + gridDim.x < batch)
-      prefetch_problem(points + (b + gridDim.x) * nd, weights + (b + gridDim.x) * n, nd, n);
+    for (int i = 0; i < J; ++i) r0[i] = greal ? st[7 * g + i] : 0.0f;
+#pragma unroll
+    for (int m = 0; m < KP; ++m) {
+      const int k0 = 2 * (m * NG + gid), k1 = k0 + 1;
+      const bool h0 = greal && k0 < n, h1 = greal && k1 < n;
+      wq[m] = make_float2(is_pts && k0 < n ? wv[k0] : 0.0f, is_pts && k1 < n ? wv[k1] : 0.0f);
+      const float* p0 = st + k0 * D + 7 * g;
+      const float* p1 = st + k1 * D + 7 * g;
+#pragma unroll
+      for (int i = 0; i < J; ++i) {
+        const float v0 = h0 ? p0[i] : r0[i], v1 = h1 ? p1[i] : r0[i];
+        neq |= (v0 != r0[i]) | (v1 != r0[i]);
+        A[m][i] = make_float2(h0 ? v0 : 0.0f, h1 ? v1 : 0.0f);
+      }
+    }
+    const float w_me = real_me ? wv[k_me] : 0.0f;
+    check_problem(A, wq, b, invalid);
+    const bool static_eq = !__syncthreads_or(neq);  // every thread is done with the stage
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t2 = clock64(); su_load += su_t2 - su_t1;
+#endif
+    const int64_t bn = b + gridDim.x;
+    if (bn < batch) {
+      stage_copy(stage, points + bn * nd, nd);
+      stage_copy(wst, weights + bn * n, n);
+    }
+    cp_commit();
     // exact stop possible (the p-form kernel decides it structurally), or the small-mu regime
     if (static_eq || all_mode) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       continue;
     }
 
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t3 = clock64(); su_pref += su_t3 - su_t2;
+#endif
     // ---- z_0 = m: z_init, or the weighted mean points * (w / sum w) (admm.hpp:40, types.hpp:73)
     float m0 = 0.0f, m1 = 0.0f;  // consensus warp: m at coordinates cj, cj + 1
-    if (z_init == nullptr) weighted_sum_rows(A, tp, wq, myrow, is_pts, lane);
+    if (z_init == nullptr) weighted_sum_rows(A, wq, myrow, is_pts, lane);
     if (warp == CW) {
       if (z_init != nullptr) {
         m0 = cv0 ? z_init[b * D + cj] : 0.0f;
@@ -464,123 +390,130 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       if (lane < 8) gr[lane] = 0.0f;
     }
     __syncthreads();
-    // centre the points on m; ||a~||^2 of this lane's two points
-    float a2[2];
+    // centre the points on m
+    float2 nq[KP];
     {
       float mc[J];
       load_coords(mb, g, mc);
-      float2 nq[KP];
 #pragma unroll
       for (int m = 0; m < KP; ++m) nq[m] = make_float2(0.0f, 0.0f);
-      auto centre = [&](int m, int i, float2 a) {
-        const int k0 = 2 * (m * NG + gid);
-        const float2 c = make_float2(greal && k0 < n ? a.x - mc[i] : 0.0f,
-                                     greal && k0 + 1 < n ? a.y - mc[i] : 0.0f);
-        nq[m] = __ffma2_rn(c, c, nq[m]);
-        return c;
-      };
 #pragma unroll
-      for (int m = 0; m < KR; ++m)
+      for (int i = 0; i < J; ++i) {
 #pragma unroll
-        for (int i = 0; i < J; ++i) A[m][i] = centre(m, i, A[m][i]);
-      if (is_pts) {
-        map_tm_half(tp, centre);
-        tm::wait_st();
+        for (int m = 0; m < KP; ++m) {
+          const int k0 = 2 * (m * NG + gid);
+          const float2 a = A[m][i];
+          A[m][i] = make_float2(greal && k0 < n ? a.x - mc[i] : 0.0f,
+                                greal && k0 + 1 < n ? a.y - mc[i] : 0.0f);
+          nq[m] = __ffma2_rn(A[m][i], A[m][i], nq[m]);
+        }
       }
-      a2[0] = group_rs8(nq, g);
-      a2[1] = group_rs8(nq + KR, g);
     }
-    // per-point state (own slots): p_1 = z_0 - a = -a~ (u = 0, admm.hpp:41)
-    float H[2], K[2], ga[2], al0[2], al1[2], al2[2], al3[2], lam[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      H[h] = a2[h];
-      K[h] = -a2[h];
-      ga[h] = al0[h] = al1[h] = al2[h] = al3[h] = 0.0f;
-      lam[h] = inv_mu * w_me[h];
-    }
+    const float a2 = group_rs8(nq, g);  // ||a~||^2 of this lane's point
+    // per-point state (own slot): p_1 = z_0 - a = -a~ (u = 0, admm.hpp:41)
+    float H = a2, K = -a2, ga = 0.0f, al0 = 0.0f, al1 = 0.0f, al2 = 0.0f, al3 = 0.0f;
+    const float lam = inv_mu * w_me;
     // consensus state (warp CW): z, history ring c~_{t-r} (r = 0..3) and its norms
     float z0 = m0, z1 = m1;
     float h0[R], h1[R], nr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) h0[r] = h1[r] = nr[r] = 0.0f;
     bool bad = false, ovf = false;
+#ifdef NLEM_BLR_STAMPS
+    long long st_wc = 0, st_wg = 0, st_a = 0, st_b1 = 0, st_cons = 0, st_q[6] = {0, 0, 0, 0, 0, 0};
+#endif
 
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t4 = clock64(); su_init += su_t4 - su_t3;
+#endif
     for (int t = 1; t <= T; ++t) {
-      if (is_pts) {
-        // (1) D_k = <a~_k, c~_t>
-        // c~_t is published by the consensus warp before its Gram row (named barriers): the dot
-        // products overlap the Gram reduction
-        if (t > 1) bar_sync(BAR_C);
-        float Dk[2];
-        {
-          float cv[J];
-          load_coords(cb, g, cv);
-          float2 dq[KP];
+     if (is_pts) {
+      // (1) D_k = <a~_k, c~_t>
+      // c~_t is published by the consensus warp before its Gram row (named barriers): the dot
+      // products overlap the Gram reduction
+      BLR_STAMP(s0);
+      if (t > 1) bar_sync(BAR_C);
+      BLR_STAMP(s1);
+      float cv[J];
+      load_coords(cb, g, cv);
+      float2 dq[KP];
 #pragma unroll
-          for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
+      for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int i = 0; i < J; ++i)
+      for (int i = 0; i < J; ++i)
 #pragma unroll
-            for (int m = 0; m < KR; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
-          for_tm_half(tp, [&](int m, int i, float2 a) { dq[m] = __ffma2_rn(a, f2(cv[i]), dq[m]); });
-          Dk[0] = group_rs8(dq, g);
-          Dk[1] = group_rs8(dq + KR, g);
-        }
-        // (2) scalar update of this lane's points
-        if (t > 1) {
-          pin[tid] = Dk[0] + Dk[1];  // the dot products and their reduction run before the wait
-          bar_sync(BAR_GRAM);
-        }
-        const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
-        const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
-        const float Gnn = gq2.x, nrR = gq2.y;
+        for (int m = 0; m < KP; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
+      BLR_STAMP(q0);
+      const float Dk = group_rs8(dq, g);
+      BLR_STAMP(q1);
+      // (2) scalar update of this lane's point
+      BLR_STAMP(s2);
+      if (t > 1) {
+        pin[tid] = Dk;  // the dot products and their reduction run before the wait
+        bar_sync(BAR_GRAM);
+      }
+      BLR_STAMP(s3);
+      const float4 gq4 = reinterpret_cast<const float4*>(gr)[0];
+      const float2 gq2 = reinterpret_cast<const float2*>(gr)[2];
+      const float Gnn = gq2.x, nrR = gq2.y;
+      const float X = fmaf(al0, gq4.x, fmaf(al1, gq4.y, fmaf(al2, gq4.z, al3 * gq4.w)));
+      const float gp1 = ga + 1.0f;
+      const float HG = H + Gnn;
+      const float N = fmaf(2.0f, fmaf(-gp1, Dk, X), HG);
+      bad |= lam != 0.0f && !isfinite(N);
+      const float Nc = fmaxf(N, 0.0f);
+      const float s = lam != 0.0f ? fminf(1.0f, lam * rsq(Nc)) : 0.0f;
+      const float Bk = K + Dk;
+      const float ev = s * al3;
+      ovf |= ev * ev * nrR > kThr2 * Nc;
+      ovf |= lam != 0.0f && N < kCancel * HG;
+      H = fmaf(s, fmaf(s, Nc, -2.0f * Bk), a2);
+      K = fmaf(s, Bk, -a2);
+      ga = s * gp1;
+      al3 = s * al2;
+      al2 = s * al1;
+      al1 = s * al0;
+      al0 = s;
+      // (3) sum_k ga'_k a~_k per coordinate; history sums sum_k al'_r (onto lanes r = 0..3)
+      BLR_STAMP(q2);
+      float2 gq[KP];
+      group_ag8(ga, gq, lane);
+      BLR_STAMP(q3);
+      float v[J];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const float X = fmaf(al0[h], gq4.x, fmaf(al1[h], gq4.y, fmaf(al2[h], gq4.z, al3[h] * gq4.w)));
-          const float gp1 = ga[h] + 1.0f;
-          const float HG = H[h] + Gnn;
-          const float N = fmaf(2.0f, fmaf(-gp1, Dk[h], X), HG);
-          bad |= lam[h] != 0.0f && !isfinite(N);
-          const float Nc = fmaxf(N, 0.0f);
-          const float s = lam[h] != 0.0f ? fminf(1.0f, lam[h] * rsq(Nc)) : 0.0f;
-          const float Bk = K[h] + Dk[h];
-          const float ev = s * al3[h];
-          ovf |= ev * ev * nrR > kThr2 * Nc;
-          ovf |= lam[h] != 0.0f && N < kCancel * HG;
-          H[h] = fmaf(s, fmaf(s, Nc, -2.0f * Bk), a2[h]);
-          K[h] = fmaf(s, Bk, -a2[h]);
-          ga[h] = s * gp1;
-          al3[h] = s * al2[h];
-          al2[h] = s * al1[h];
-          al1[h] = s * al0[h];
-          al0[h] = s;
-        }
-        // (3) sum_k ga'_k a~_k per coordinate; history sums sum_k al'_r (onto lanes r = 0..3)
-        float v[J];
-        {
-          float2 acc[J];
+      for (int i = 0; i < J; ++i) {
+        float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int i = 0; i < J; ++i) acc[i] = make_float2(0.0f, 0.0f);
-          float2 gq[KP];
-          group_ag8(ga[0], gq, lane);
-          group_ag8(ga[1], gq + KR, lane);
+        for (int m = 0; m < KP; ++m) acc = __ffma2_rn(gq[m], A[m][i], acc);
+        v[i] = acc.x + acc.y;
+      }
+      BLR_STAMP(q4);
+      float hs;
+      {
+        const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
+        const float x0 = (u2 ? al2 : al0) + __shfl_xor_sync(0xffffffffu, u2 ? al0 : al2, 2);
+        const float x1 = (u2 ? al3 : al1) + __shfl_xor_sync(0xffffffffu, u2 ? al1 : al3, 2);
+        hs = (u1 ? x1 : x0) + __shfl_xor_sync(0xffffffffu, u1 ? x0 : x1, 1);
 #pragma unroll
-          for (int m = 0; m < KR; ++m)
-#pragma unroll
-            for (int i = 0; i < J; ++i) acc[i] = __ffma2_rn(gq[m], A[m][i], acc[i]);
-          for_tm_half(tp, [&](int m, int i, float2 a) { acc[i] = __ffma2_rn(gq[m], a, acc[i]); });
-#pragma unroll
-          for (int i = 0; i < J; ++i) v[i] = acc[i].x + acc[i].y;
-        }
-        const float hs = quad_sums(al0[0] + al0[1], al1[0] + al1[1], al2[0] + al2[1],
-                                   al3[0] + al3[1], lane);
-        fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
-        __syncthreads();
-      } else {
-        __syncthreads();
-        // (4) consensus (warp CW): z_t = P_C(z_{t-1} - g/n), c~_{t+1} = 2 z_t - z_{t-1} - m, and
-        // the Gram row of sweep t+1
+        for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+      }
+      fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
+      BLR_STAMP(s4);
+      __syncthreads();
+      BLR_STAMP(s5);
+#ifdef NLEM_BLR_STAMPS
+      st_wc += s1 - s0; st_wg += s3 - s2; st_a += (s4 - s1) - (s3 - s2); st_b1 += s5 - s4;
+      st_q[0] += q0 - s1; st_q[1] += q1 - q0; st_q[2] += q2 - s3; st_q[3] += q3 - q2; st_q[4] += q4 - q3; st_q[5] += s4 - q4;
+#endif
+     } else {
+      BLR_STAMP(s4);
+      __syncthreads();
+      BLR_STAMP(s5);
+#ifdef NLEM_BLR_STAMPS
+      st_b1 += s5 - s4;
+#endif
+      // (4) consensus (warp CW): z_t = P_C(z_{t-1} - g/n), c~_{t+1} = 2 z_t - z_{t-1} - m, and
+      // the Gram row of sweep t+1
         const float2 S = rows_sum(red, lane);
         float As[R];
 #pragma unroll
@@ -627,9 +560,24 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         }
         __syncwarp();
         if (t < T) bar_arrive(BAR_GRAM);
-      }
+#ifdef NLEM_BLR_STAMPS
+        BLR_STAMP(s6);
+        st_cons += s6 - s5;
+#endif
+     }
     }
 
+#ifdef NLEM_BLR_STAMPS
+    if (blockIdx.x == 0 && b < 3 * gridDim.x && (tid == 0 || tid == 32 || tid == CW * 32))
+      printf("blr stamps warp %d T %d: wait_c %lld wait_gram %lld phaseA %lld wait_b1 %lld cons %lld (per sweep)\n",
+             warp, T, st_wc / T, st_wg / T, st_a / T, st_b1 / T, st_cons / T);
+    if (blockIdx.x == 0 && b < 3 * gridDim.x && tid == 32)
+      printf("blr phaseA: dot %lld rs8 %lld scalar %lld ag8 %lld wsum %lld fold+hs+sts %lld\n", st_q[0] / T,
+             st_q[1] / T, st_q[2] / T, st_q[3] / T, st_q[4] / T, st_q[5] / T);
+#endif
+#ifdef NLEM_BLR_STAMPS
+    const long long su_t5 = clock64(); su_sw += su_t5 - su_t4;
+#endif
     // ---- hand-off or outputs
     if (__syncthreads_or(bad || ovf)) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
@@ -649,46 +597,54 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       float2 dq[KP];
 #pragma unroll
       for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
-      auto dist = [&](int m, int i, float2 a) {
-        const float2 e = __fadd2_rn(f2(zc[i]), make_float2(-a.x, -a.y));
-        const float2 em = 7 * g + i < D ? e : make_float2(0.0f, 0.0f);
-        dq[m] = __ffma2_rn(em, em, dq[m]);
-      };
 #pragma unroll
-      for (int m = 0; m < KR; ++m)
+      for (int i = 0; i < J; ++i) {
+        const bool jr = 7 * g + i < D;
 #pragma unroll
-        for (int i = 0; i < J; ++i) dist(m, i, A[m][i]);
-      if (is_pts) for_tm_half(tp, dist);
-      const float d0 = group_rs8(dq, g), d1 = group_rs8(dq + KR, g);
-      const float mine = (real_me[0] ? w_me[0] * sqrtf(d0) : 0.0f) +
-                         (real_me[1] ? w_me[1] * sqrtf(d1) : 0.0f);
-      const float obj = block_sum0(mine, scal, warp, lane);
+        for (int m = 0; m < KP; ++m) {
+          const float2 e = __fadd2_rn(f2(zc[i]), make_float2(-A[m][i].x, -A[m][i].y));
+          const float2 em = jr ? e : make_float2(0.0f, 0.0f);
+          dq[m] = __ffma2_rn(em, em, dq[m]);
+        }
+      }
+      const float dist2 = group_rs8(dq, g);
+      const float obj = block_sum0(real_me ? w_me * sqrtf(dist2) : 0.0f, scal, warp, lane);
       if (tid == 0) {
         obj_out[b] = obj;
         if (!isfinite(obj)) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       }
     }
+#ifdef NLEM_BLR_STAMPS
+    { const long long e_ = clock64(); su_epi += e_ - su_t5; ++su_n; }
+#endif
   }
-  tm::dealloc_cta<TM_COLS>(tbase, warp);
+#ifdef NLEM_BLR_STAMPS
+  if (blockIdx.x < 2 && (tid == 0 || tid == CW * 32) && su_n)
+    printf("blr setup blk %d warp %d: problems %lld wait %lld load %lld prefetch %lld init %lld sweeps %lld epilogue %lld\n",
+           blockIdx.x, warp, su_n, su_wait / su_n, su_load / su_n, su_pref / su_n, su_init / su_n,
+           su_sw / su_n, su_epi / su_n);
+#endif
+  cp_wait_all();
 }
 
 // ---------------------------------------------------------------------------------------
-// Batched IRLS (proj/include/nlem/irls.hpp:21-68), d = 49, 1 <= n <= 448: the same layout
-// (half of the points in registers, half in tensor memory, two problems per SM) and consensus
-// warp, direct differences (exact near coincident points, where epsilon matters).  Pass p
-// evaluates at x_p: per point D = ||x_p - a_k||^2 (FADD2 + FFMA2), root = sqrt(D + eps), beta =
-// w / root, the surrogate term w root (costs.hpp:24-33) and the cost term w sqrt(D)
-// (costs.hpp:13-20, the objective output at the final x); the point warps reduce sum beta a,
-// sum beta, the surrogate and the cost; the consensus warp applies the stop rule (irls.hpp:58)
-// and forms x_{p+1} = sum beta a / sum beta.  Failures are recorded as the generic kernel does
-// (iteration and kind of irls.hpp:39, :50, :52, :65-66).
+// Batched IRLS (proj/include/nlem/irls.hpp:21-68), d = 49, 1 <= n <= 448: the same register
+// layout and consensus warp, direct differences (exact near coincident points, where epsilon
+// matters).  Pass p evaluates at x_p: per point D = ||x_p - a_k||^2 (FADD2 + FFMA2), root =
+// sqrt(D + eps), beta = w / root, the surrogate term w root (costs.hpp:24-33) and the cost term
+// w sqrt(D) (costs.hpp:13-20, the objective output at the final x); the point warps reduce
+// sum beta a, sum beta, the surrogate and the cost; the consensus warp applies the stop rule
+// (irls.hpp:58) and forms x_{p+1} = sum beta a / sum beta.  Failures are recorded as the
+// generic kernel does (iteration and kind of irls.hpp:39, :50, :52, :65-66).
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(ALL, 2)
+__global__ void __launch_bounds__(ALL, 1)
 irls_batched_reg(const float* __restrict__ points, const float* __restrict__ weights,
                  int64_t batch, int n, const float* __restrict__ x_init, float eps, int T,
                  float tol, float* x_out, float* obj_out, int* iters_out, float* tr_obj,
                  FailureSlot* fail, unsigned long long* invalid) {
   extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
   float* const red = smem + SM_RED;
   float* const cb = smem + SM_CB;  // x of the coming pass
   int* const ctl = reinterpret_cast<int*>(smem + SM_GR);
@@ -698,38 +654,52 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   const int g = lane & (G - 1);
   const int gid = warp * GPW + (lane >> 3);
   const bool is_pts = warp < WARPS;
-  // TMEM: the second half of every lane's points (128 columns per CTA, two CTAs per SM)
-  const uint32_t tbase = tm::alloc_cta<TM_COLS>(reinterpret_cast<uint32_t*>(smem + SM_TB), warp);
-  const uint32_t tp = tm::warp_addr(tbase, warp, (warp >> 2) * TM_WCOLS);
   float* const myrow = red + (is_pts ? warp : 0) * RS;
-  int k_me[2];
-  bool real_me[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    k_me[h] = 2 * ((KR * h + (g >> 1)) * NG + gid) + (g & 1);
-    real_me[h] = is_pts && k_me[h] < n;
-  }
+  auto point_of = [&](int q) { return 2 * ((q >> 1) * NG + gid) + (q & 1); };
+  const int k_me = point_of(g);
+  const bool real_me = is_pts && k_me < n;
   const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
   const int cj = 7 * cgrp + cidx;
   const bool cv0 = cgrp < 7, cv1 = cgrp < 7 && (lane & 3) != 3;
   const int nd = n * D;
 
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    const float* const src = points + b * nd;
-    const float* const wsrc = weights + b * n;
-    float2 A[KR][J];
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+
+  for (; b < batch; b += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();
+    const float* const st = stage + stage_shift(points + b * nd);
+    const float* const wv = wst + stage_shift(weights + b * n);
+    const bool greal = is_pts && g < 7;
+    float2 A[KP][J];
     float2 wq[KP];
-    const Loaded ld = load_problem(src, wsrc, n, gid, g, is_pts, A, wq, tp);
-    float w_me[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? __ldg(wsrc + k_me[h]) : 0.0f;
-    check_problem(ld.bad_pt, wq, b, invalid);
-    __syncthreads();  // every warp is past the previous problem's ctl / row reads
-    if (b + gridDim.x < batch)
-      prefetch_problem(points + (b + gridDim.x) * nd, weights + (b + gridDim.x) * n, nd, n);
+    for (int m = 0; m < KP; ++m) {
+      const int k0 = 2 * (m * NG + gid), k1 = k0 + 1;
+      const bool h0 = greal && k0 < n, h1 = greal && k1 < n;
+      wq[m] = make_float2(is_pts && k0 < n ? wv[k0] : 0.0f, is_pts && k1 < n ? wv[k1] : 0.0f);
+      const float* p0 = st + k0 * D + 7 * g;
+      const float* p1 = st + k1 * D + 7 * g;
+#pragma unroll
+      for (int i = 0; i < J; ++i) A[m][i] = make_float2(h0 ? p0[i] : 0.0f, h1 ? p1[i] : 0.0f);
+    }
+    const float w_me = real_me ? wv[k_me] : 0.0f;
+    check_problem(A, wq, b, invalid);
+    __syncthreads();  // every thread is done with the stage
+    const int64_t bn = b + gridDim.x;
+    if (bn < batch) {
+      stage_copy(stage, points + bn * nd, nd);
+      stage_copy(wst, weights + bn * n, n);
+    }
+    cp_commit();
 
     // ---- x_0: x_init, or the weighted mean points * (w / sum w) (irls.hpp:32, types.hpp:73)
-    if (x_init == nullptr) weighted_sum_rows(A, tp, wq, myrow, is_pts, lane);
+    if (x_init == nullptr) weighted_sum_rows(A, wq, myrow, is_pts, lane);
     float x0 = 0.0f, x1 = 0.0f;  // consensus warp: x of the current pass at cj, cj + 1
     if (warp == CW) {
       if (x_init != nullptr) {
@@ -754,47 +724,43 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
         float2 dq[KP];
 #pragma unroll
         for (int m = 0; m < KP; ++m) dq[m] = make_float2(0.0f, 0.0f);
-        // no mask for the padding coordinates of lanes g = 7: their points are 0 and x's
-        // padding columns are written as exact zeros (cv0 / cv1), so e = 0 there
-        auto dist = [&](int m, int i, float2 a) {
-          const float2 e = __fadd2_rn(f2(xc[i]), make_float2(-a.x, -a.y));
-          dq[m] = __ffma2_rn(e, e, dq[m]);
-        };
 #pragma unroll
-        for (int i = 0; i < J; ++i)
+        for (int i = 0; i < J; ++i) {
 #pragma unroll
-          for (int m = 0; m < KR; ++m) dist(m, i, A[m][i]);
-        for_tm_half(tp, dist);
-        float d2[2] = {group_rs8(dq, g), group_rs8(dq + KR, g)};
+          for (int m = 0; m < KP; ++m) {
+            // no mask for the padding coordinates of lanes g = 7: their points are 0 and x's
+            // padding columns are written as exact zeros (cv0 / cv1), so e = 0 there
+            const float2 e = __fadd2_rn(f2(xc[i]), make_float2(-A[m][i].x, -A[m][i].y));
+            dq[m] = __ffma2_rn(e, e, dq[m]);
+          }
+        }
+        const float d2 = group_rs8(dq, g);
         // irls.hpp:45-46 and costs.hpp:24-33 / :13-20 with one hardware reciprocal square root
         // per point each (rsqrt.approx: ~2 ulp, against an FP64 reference)
-        float beta[2], sur = 0.0f, cost = 0.0f;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const float s2 = d2[h] + eps;
-          const float ri = rsq(s2);
-          beta[h] = real_me[h] ? w_me[h] * ri : 0.0f;
-          sur += real_me[h] ? w_me[h] * (s2 * ri) : 0.0f;
-          cost += real_me[h] && d2[h] > 0.0f ? w_me[h] * (d2[h] * rsq(d2[h])) : 0.0f;
-        }
+        const float s2 = d2 + eps;
+        const float ri = rsq(s2);
+        const float beta = real_me ? w_me * ri : 0.0f;
+        const float sur = real_me ? w_me * (s2 * ri) : 0.0f;
+        const float cost = real_me && d2 > 0.0f ? w_me * (d2 * rsq(d2)) : 0.0f;
+        float2 bq[KP];
+        group_ag8(beta, bq, lane);
         float v[J];
-        {
-          float2 acc[J];
 #pragma unroll
-          for (int i = 0; i < J; ++i) acc[i] = make_float2(0.0f, 0.0f);
-          float2 bq[KP];
-          group_ag8(beta[0], bq, lane);
-          group_ag8(beta[1], bq + KR, lane);
+        for (int i = 0; i < J; ++i) {
+          float2 acc = make_float2(0.0f, 0.0f);
 #pragma unroll
-          for (int m = 0; m < KR; ++m)
-#pragma unroll
-            for (int i = 0; i < J; ++i) acc[i] = __ffma2_rn(bq[m], A[m][i], acc[i]);
-          for_tm_half(tp, [&](int m, int i, float2 a) { acc[i] = __ffma2_rn(bq[m], a, acc[i]); });
-#pragma unroll
-          for (int i = 0; i < J; ++i) v[i] = acc[i].x + acc[i].y;
+          for (int m = 0; m < KP; ++m) acc = __ffma2_rn(bq[m], A[m][i], acc);
+          v[i] = acc.x + acc.y;
         }
-        // warp sums of (beta, surrogate, cost, 0) onto lanes r = lane & 3
-        const float hs = quad_sums(beta[0] + beta[1], sur, cost, 0.0f, lane);
+        float hs;  // warp sums of (beta, surrogate, cost, 0) onto lanes r = lane & 3
+        {
+          const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
+          const float x0_ = (u2 ? cost : beta) + __shfl_xor_sync(0xffffffffu, u2 ? beta : cost, 2);
+          const float x1_ = (u2 ? 0.0f : sur) + __shfl_xor_sync(0xffffffffu, u2 ? sur : 0.0f, 2);
+          hs = (u1 ? x1_ : x0_) + __shfl_xor_sync(0xffffffffu, u1 ? x0_ : x1_, 1);
+#pragma unroll
+          for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+        }
         fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
       }
       __syncthreads();
@@ -860,13 +826,8 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
       }
     }
   }
-  tm::dealloc_cta<TM_COLS>(tbase, warp);
+  cp_wait_all();
 }
-
-// persistent grid: two CTAs per SM (registers: 2 x 256 threads x 128; shared memory below)
-constexpr int kCtasPerSm = 2;
-constexpr int kCarveoutPct =
-    static_cast<int>((kCtasPerSm * (SMEM_BYTES + 1024) * 100 + 233471) / 233472) + 2;
 
 bool irls_reg_supported(const IrlsLaunch& L) {
   const char* force = std::getenv("NLEM_BATCHED");  // =fast: the generic IRLS kernel (A/B, tests)
@@ -880,10 +841,7 @@ cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  // shared-memory carve-out for kCtasPerSm resident CTAs (the rest of the 256 KB stays L1)
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, kCarveoutPct);
-  if (e != cudaSuccess) return e;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, int64_t(kCtasPerSm) * device_caps().sms));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.x_init, L.eps, L.max_iter, L.tol, L.x_out, L.obj_out,
       L.iters_out, L.tr_obj, L.fail, L.invalid);
@@ -957,9 +915,6 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
-  // shared-memory carve-out for kCtasPerSm resident CTAs (the rest of the 256 KB stays L1)
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, kCarveoutPct);
-  if (e != cudaSuccess) return e;
   if (probe != nullptr && L.max_iter > R) {
     const int pn = static_cast<int>(std::min<int64_t>(L.batch, kProbe));
     small_mu_probe_kernel<<<pn, 256, 0, stream>>>(L.points, L.weights, L.batch, L.n, L.z_init,
@@ -968,12 +923,7 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int
   } else {
     probe = nullptr;
   }
-  if (std::getenv("NLEM_LR_STATS") != nullptr) {  // diagnostics only
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, ALL, SMEM_BYTES);
-    std::fprintf(stderr, "admm_batched_lr: %d resident CTAs per SM\n", occ);
-  }
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, int64_t(kCtasPerSm) * device_caps().sms));
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, device_caps().sms));
   kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
       L.points, L.weights, L.batch, L.n, L.z_init, L.box, L.mu, L.max_iter, L.z_out, L.obj_out,
       L.iters_out, ho_list, ho_count, L.invalid, probe);
