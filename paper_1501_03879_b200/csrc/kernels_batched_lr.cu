@@ -40,8 +40,8 @@
 //    (named barrier 1) and then the Gram row (named barrier 2), so the point warps' dot products
 //    overlap the Gram reduction; ptxas moves arithmetic across bar.sync, so the order is pinned
 //    with a shared-memory store before each wait and a reload after the arrive;
-//  * points are read straight from HBM / L2 at the start of a problem (the next problem's lines
-//    are prefetched into L2 during the sweeps); the co-resident CTA hides the latency.
+//  * the next problem's points and weights stream into a shared-memory staging buffer with
+//    16-byte cp.async during the current problem's sweeps (88 KB per CTA).
 // The batched IRLS kernel (irls_batched_reg, below) reuses the layout and the consensus warp.
 #include <algorithm>
 #include <cstdint>
@@ -75,7 +75,9 @@ constexpr float kThr2 = 1.0f / 17592186044416.0f;  // (2^-22)^2: ring term below
 constexpr float kCancel = 1.0f / 256.0f;           // N below 2^-8 (H + ||c~||^2): cancellation
 constexpr int kProbe = 64;                         // problems sampled by the small-mu probe
 // shared memory (floats)
-constexpr int SM_RED = 0;                        // [WARPS][RS] per-warp partial rows
+constexpr int SM_STAGE = 0;                      // raw points of the next problem (+4 shift)
+constexpr int SM_WST = SM_STAGE + NCAP * D + 4;  // raw weights of the next problem (+4 shift)
+constexpr int SM_RED = SM_WST + NCAP + 4;        // [WARPS][RS] per-warp partial rows
 // Published rows (c~ / x, m) are read by every point lane as two 16-byte loads at column 8 g:
 // columns 32..63 sit 4 floats further on (RSK = RS + 4), so lanes g and g + 4 hit distinct banks
 // (one wavefront per load instead of two; these loads follow the row barrier on every warp).
@@ -90,7 +92,7 @@ constexpr int SM_TOTAL = SM_TB + 4;
 constexpr size_t SMEM_BYTES = size_t(SM_TOTAL) * sizeof(float);
 static_assert(NCAP >= 441, "config-1 capacity");
 static_assert(TM_HALF == 56 && TM_HALF <= TM_WCOLS && 2 * TM_WCOLS <= TM_COLS, "TMEM layout");
-static_assert(SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_MB % 4 == 0 && SM_GR % 4 == 0, "alignment");
+static_assert(SM_WST % 4 == 0 && SM_RED % 4 == 0 && SM_CB % 4 == 0 && SM_MB % 4 == 0 && SM_GR % 4 == 0, "alignment");
 static_assert(2 * (SMEM_BYTES + 1024) <= 233472, "two CTAs per SM");
 
 __device__ __forceinline__ float rsq(float x) {
@@ -99,8 +101,35 @@ __device__ __forceinline__ float rsq(float x) {
   return y;
 }
 __device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+__device__ __forceinline__ void cp16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tm::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(tm::smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+// element e of `src` lands at dst[shift(src) + e], shift = (src / 4) mod 4, so that global and
+// shared addresses agree mod 16 and the interior moves as 16-byte cp.async
+__device__ __forceinline__ int stage_shift(const float* src) {
+  return static_cast<int>((reinterpret_cast<uintptr_t>(src) >> 2) & 3);
+}
+__device__ __forceinline__ void stage_copy(float* dst, const float* src, int total) {
+  const int s0 = stage_shift(src);
+  const int nch = (s0 + total + 3) >> 2;
+  const float* base = src - s0;  // 16-byte aligned
+  for (int c = threadIdx.x; c < nch; c += ALL) {
+    const int e0 = 4 * c - s0;
+    if (e0 >= 0 && e0 + 3 < total) {
+      cp16(dst + 4 * c, base + 4 * c);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = e0 + q;
+        if (e >= 0 && e < total) cp4(dst + 4 * c + q, base + 4 * c + q);
+      }
+    }
+  }
 }
 // named barriers: the consensus warp arrives, the other warps wait (count = all threads)
 __device__ __forceinline__ void bar_sync(int id) {
@@ -184,34 +213,36 @@ __device__ __forceinline__ void map_tm_half(uint32_t tp, F&& f) {
   tm::st8<48>(tp, v);
 }
 
-// Reduce-scatter of 8 per-point values (4 float2 slots) across the 8 lanes of a group: lane g
-// returns the sum for point slot g.  Fixed tree (bitwise deterministic).
-__device__ __forceinline__ float group_rs8(const float2* v, int g) {
-  float x[G];
-#pragma unroll
-  for (int m = 0; m < G / 2; ++m) {
-    x[2 * m] = v[m].x;
-    x[2 * m + 1] = v[m].y;
-  }
-#pragma unroll
-  for (int half = G / 2; half >= 1; half >>= 1) {
-    const bool up = (g & half) != 0;
-#pragma unroll
-    for (int i = 0; i < half; ++i) {
-      const float keep = up ? x[i + half] : x[i];
-      const float send = up ? x[i] : x[i + half];
-      x[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
-    }
-  }
-  return x[0];
+// Slot layout inside a group (XOR-relative): register slot q (pair q / 2, side q & 1) of lane g
+// holds the data of the group's point slot q ^ g (of either half), so the recursive-halving
+// reduce-scatter keeps and sends STATIC registers (no per-lane selects) and lane g ends up
+// with the sum of point slot g in register slot 0; the all-gather is shfl_xor by q.
+// First of the two points (sides x, y) of register pair m (0..KP-1) on lane g of group gid; the
+// second is k0 ^ 1.
+__device__ __forceinline__ int pair_point0(int m, int g, int gid) {
+  const int s0 = (2 * (m % KR)) ^ g;  // point slot of side x
+  return 2 * (((m / KR) * KR + (s0 >> 1)) * NG + gid) + (s0 & 1);
 }
-// All-gather of one value per lane of the group into 4 float2 slots (slot 2m, 2m+1).
-__device__ __forceinline__ void group_ag8(float mine, float2* out, int lane) {
-  const int base = lane & ~(G - 1);
+__device__ __forceinline__ float2 shfl_xor2(float2 v, int mask) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, v.x, mask), __shfl_xor_sync(0xffffffffu, v.y, mask));
+}
+// Reduce-scatter of 8 per-point values (4 float2 register pairs) across the 8 lanes of a group:
+// lane g returns the sum for point slot g.  Fixed tree (bitwise deterministic).
+__device__ __forceinline__ float group_rs8(const float2* v) {
+  float2 a0 = __fadd2_rn(v[0], shfl_xor2(v[2], 4));
+  const float2 a1 = __fadd2_rn(v[1], shfl_xor2(v[3], 4));
+  a0 = __fadd2_rn(a0, shfl_xor2(a1, 2));
+  return a0.x + __shfl_xor_sync(0xffffffffu, a0.y, 1);
+}
+// All-gather of one value per lane of the group into 4 float2 register pairs: register slot q
+// receives the value of point slot q ^ g, owned by lane g ^ q.
+__device__ __forceinline__ void group_ag8(float mine, float2* out) {
+  out[0].x = mine;
+  out[0].y = __shfl_xor_sync(0xffffffffu, mine, 1);
 #pragma unroll
-  for (int m = 0; m < G / 2; ++m) {
-    out[m].x = __shfl_sync(0xffffffffu, mine, base + 2 * m);
-    out[m].y = __shfl_sync(0xffffffffu, mine, base + 2 * m + 1);
+  for (int m = 1; m < G / 2; ++m) {
+    out[m].x = __shfl_xor_sync(0xffffffffu, mine, 2 * m);
+    out[m].y = __shfl_xor_sync(0xffffffffu, mine, 2 * m + 1);
   }
 }
 // Sum the 7 per-lane column partials over the 4 groups of the warp (lanes of group 0 then
@@ -268,8 +299,8 @@ __device__ __forceinline__ float block_sum0(float v, float* scal, int warp, int 
   return t;
 }
 
-// One problem's points and weights from global memory: pairs 0..KR-1 into registers, pairs KR..
-// into this lane's TMEM columns (raw), with the fused input validation (types.hpp:58-68, the
+// One problem's points and weights from the shared-memory stage: pairs 0..KR-1 into registers,
+// pairs KR.. into this lane's TMEM columns (raw), with the fused input validation (types.hpp:58-68, the
 // checks validate_points_dev runs as a separate pass) and the all-points-equal test.  Padding
 // slots (k >= n, coordinates >= 49) hold finite 0.  Returns (any element != point 0's).
 struct Loaded {
@@ -283,13 +314,13 @@ __device__ __forceinline__ Loaded load_problem(const float* __restrict__ src,
   const float* const col = src + 7 * g;
   float r0[J];
 #pragma unroll
-  for (int i = 0; i < J; ++i) r0[i] = greal ? __ldg(col + i) : 0.0f;
+  for (int i = 0; i < J; ++i) r0[i] = greal ? col[i] : 0.0f;
   bool bad = false, neq = false;
   auto fetch = [&](int m, int i) {
-    const int k0 = 2 * (m * NG + gid);
-    const bool h0 = greal && k0 < n, h1 = greal && k0 + 1 < n;
-    const float v0 = h0 ? __ldg(col + k0 * D + i) : r0[i];
-    const float v1 = h1 ? __ldg(col + (k0 + 1) * D + i) : r0[i];
+    const int k0 = pair_point0(m, g, gid), k1 = k0 ^ 1;
+    const bool h0 = greal && k0 < n, h1 = greal && k1 < n;
+    const float v0 = h0 ? col[k0 * D + i] : r0[i];
+    const float v1 = h1 ? col[k1 * D + i] : r0[i];
     neq |= (v0 != r0[i]) | (v1 != r0[i]);
     bad |= !isfinite(v0) | !isfinite(v1);
     return make_float2(h0 ? v0 : 0.0f, h1 ? v1 : 0.0f);
@@ -304,9 +335,8 @@ __device__ __forceinline__ Loaded load_problem(const float* __restrict__ src,
     for (int i = 0; i < J; ++i) A[m][i] = fetch(m, i);
 #pragma unroll
   for (int m = 0; m < KP; ++m) {
-    const int k0 = 2 * (m * NG + gid);
-    wq[m] = make_float2(is_pts && k0 < n ? __ldg(wsrc + k0) : 0.0f,
-                        is_pts && k0 + 1 < n ? __ldg(wsrc + k0 + 1) : 0.0f);
+    const int k0 = pair_point0(m, g, gid), k1 = k0 ^ 1;
+    wq[m] = make_float2(is_pts && k0 < n ? wsrc[k0] : 0.0f, is_pts && k1 < n ? wsrc[k1] : 0.0f);
   }
   return Loaded{bad, neq};
 }
@@ -326,15 +356,6 @@ __device__ __forceinline__ void check_problem(bool bad_pt, const float2 (&wq)[KP
   if (bad_w) atomicMin(invalid, key | 2ull);
   if (!__syncthreads_or(pos) && threadIdx.x == 0) atomicMin(invalid, key | 3ull);
 }
-// the lines of one problem into L2 (128-byte steps over points and weights)
-__device__ __forceinline__ void prefetch_problem(const float* src, const float* wsrc, int nd,
-                                                 int n) {
-  const char* p = reinterpret_cast<const char*>(src);
-  for (int o = threadIdx.x * 128; o < nd * 4; o += ALL * 128) prefetch_l2(p + o);
-  const char* w = reinterpret_cast<const char*>(wsrc);
-  for (int o = threadIdx.x * 128; o < n * 4; o += ALL * 128) prefetch_l2(w + o);
-}
-
 // Weighted-mean numerator and denominator in one row pass (admm.hpp:40 / irls.hpp:32 with
 // types.hpp:71-74): the point warps write sum_k w_k a_k per coordinate and the weight sum (column
 // 7) into their partial rows; one barrier; the consensus warp divides (sum w a) / (sum w).
@@ -392,6 +413,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const bool all_mode =
       probe_count != nullptr && 10 * static_cast<int64_t>(*static_cast<const volatile int*>(probe_count)) > 9 * pt;
   extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
   float* const red = smem + SM_RED;
   float* const cb = smem + SM_CB;
   float* const mb = smem + SM_MB;
@@ -409,12 +432,12 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const uint32_t tp = tm::warp_addr(tbase, warp, (warp >> 2) * TM_WCOLS);
   float* const myrow = red + (is_pts ? warp : 0) * RS;
   const bool greal = is_pts && g < 7;
-  // this lane's two point slots: slot h is side g & 1 of pair KR h + g / 2
+  // this lane's two point slots: point slot g of each half (its register slot 0)
   int k_me[2];
   bool real_me[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    k_me[h] = 2 * ((KR * h + (g >> 1)) * NG + gid) + (g & 1);
+    k_me[h] = pair_point0(KR * h, g, gid);  // register slot 0 = point slot g
     real_me[h] = is_pts && k_me[h] < n;
   }
   // consensus (warp CW): lane l finishes columns 2l, 2l+1 = coordinates cj, cj + 1
@@ -425,21 +448,31 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
   const float inv_n = 1.0f / static_cast<float>(n);
   const int nd = n * D;
 
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    // ---- this problem's points (raw) into registers / smem, weights, all-equal test
-    const float* const src = points + b * nd;
-    const float* const wsrc = weights + b * n;
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+  for (; b < batch; b += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();
+    // ---- this problem's points (raw) into registers / TMEM, weights, all-equal test
+    const float* const src = stage + stage_shift(points + b * nd);
+    const float* const wsrc = wst + stage_shift(weights + b * n);
     float2 A[KR][J];
     float2 wq[KP];
     const Loaded ld = load_problem(src, wsrc, n, gid, g, is_pts, A, wq, tp);
     float w_me[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? __ldg(wsrc + k_me[h]) : 0.0f;
+    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? wsrc[k_me[h]] : 0.0f;
     check_problem(ld.bad_pt, wq, b, invalid);
-    // every warp is past the previous problem (its pin / scal / mb reads) after this barrier
-    const bool static_eq = !__syncthreads_or(ld.neq);
-    if (b + gridDim.x < batch)
-      prefetch_problem(points + (b + gridDim.x) * nd, weights + (b + gridDim.x) * n, nd, n);
+    const bool static_eq = !__syncthreads_or(ld.neq);  // every thread is done with the stage
+    if (b + gridDim.x < batch) {  // the next problem streams in during this one's sweeps
+      stage_copy(stage, points + (b + gridDim.x) * nd, nd);
+      stage_copy(wst, weights + (b + gridDim.x) * n, n);
+    }
+    cp_commit();
     // exact stop possible (the p-form kernel decides it structurally), or the small-mu regime
     if (static_eq || all_mode) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
@@ -473,9 +506,9 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #pragma unroll
       for (int m = 0; m < KP; ++m) nq[m] = make_float2(0.0f, 0.0f);
       auto centre = [&](int m, int i, float2 a) {
-        const int k0 = 2 * (m * NG + gid);
+        const int k0 = pair_point0(m, g, gid);
         const float2 c = make_float2(greal && k0 < n ? a.x - mc[i] : 0.0f,
-                                     greal && k0 + 1 < n ? a.y - mc[i] : 0.0f);
+                                     greal && (k0 ^ 1) < n ? a.y - mc[i] : 0.0f);
         nq[m] = __ffma2_rn(c, c, nq[m]);
         return c;
       };
@@ -487,8 +520,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
         map_tm_half(tp, centre);
         tm::wait_st();
       }
-      a2[0] = group_rs8(nq, g);
-      a2[1] = group_rs8(nq + KR, g);
+      a2[0] = group_rs8(nq);
+      a2[1] = group_rs8(nq + KR);
     }
     // per-point state (own slots): p_1 = z_0 - a = -a~ (u = 0, admm.hpp:41)
     float H[2], K[2], ga[2], al0[2], al1[2], al2[2], al3[2], lam[2];
@@ -504,7 +537,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     float h0[R], h1[R], nr[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) h0[r] = h1[r] = nr[r] = 0.0f;
-    bool bad = false, ovf = false;
+    bool bad = false;  // consensus warp: non-finite iterate
+    float hov = 0.0f;  // point lanes: running maximum of the hand-off tests
 
     for (int t = 1; t <= T; ++t) {
       if (is_pts) {
@@ -524,8 +558,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #pragma unroll
             for (int m = 0; m < KR; ++m) dq[m] = __ffma2_rn(A[m][i], f2(cv[i]), dq[m]);
           for_tm_half(tp, [&](int m, int i, float2 a) { dq[m] = __ffma2_rn(a, f2(cv[i]), dq[m]); });
-          Dk[0] = group_rs8(dq, g);
-          Dk[1] = group_rs8(dq + KR, g);
+          Dk[0] = group_rs8(dq);
+          Dk[1] = group_rs8(dq + KR);
         }
         // (2) scalar update of this lane's points
         if (t > 1) {
@@ -541,14 +575,17 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
           const float gp1 = ga[h] + 1.0f;
           const float HG = H[h] + Gnn;
           const float N = fmaf(2.0f, fmaf(-gp1, Dk[h], X), HG);
-          bad |= lam[h] != 0.0f && !isfinite(N);
           const float Nc = fmaxf(N, 0.0f);
           const float s = lam[h] != 0.0f ? fminf(1.0f, lam[h] * rsq(Nc)) : 0.0f;
           const float Bk = K[h] + Dk[h];
           const float ev = s * al3[h];
-          ovf |= ev * ev * nrR > kThr2 * Nc;
-          ovf |= lam[h] != 0.0f && N < kCancel * HG;
-          H[h] = fmaf(s, fmaf(s, Nc, -2.0f * Bk), a2[h]);
+          // hand-off tests as one running maximum (> 0: hand off): a dropped ring term above
+          // rounding, or a cancelling N (zero-weight points included: a spurious hand-off only
+          // costs time)
+          hov = fmaxf(hov, fmaxf(fmaf(ev * ev, nrR, -kThr2 * Nc), fmaf(kCancel, HG, -N)));
+          // N unclamped: a non-finite N (or D) makes H non-finite for good, tested after the
+          // last sweep instead of every sweep
+          H[h] = fmaf(s, fmaf(s, N, -2.0f * Bk), a2[h]);
           K[h] = fmaf(s, Bk, -a2[h]);
           ga[h] = s * gp1;
           al3[h] = s * al2[h];
@@ -563,8 +600,8 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #pragma unroll
           for (int i = 0; i < J; ++i) acc[i] = make_float2(0.0f, 0.0f);
           float2 gq[KP];
-          group_ag8(ga[0], gq, lane);
-          group_ag8(ga[1], gq + KR, lane);
+          group_ag8(ga[0], gq);
+          group_ag8(ga[1], gq + KR);
 #pragma unroll
           for (int m = 0; m < KR; ++m)
 #pragma unroll
@@ -631,7 +668,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
     }
 
     // ---- hand-off or outputs
-    if (__syncthreads_or(bad || ovf)) {
+    if (__syncthreads_or(bad || hov > 0.0f || !isfinite(H[0]) || !isfinite(H[1]))) {
       if (tid == 0) ho_list[atomicAdd(ho_count, 1)] = static_cast<int>(b);
       continue;
     }
@@ -659,7 +696,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 #pragma unroll
         for (int i = 0; i < J; ++i) dist(m, i, A[m][i]);
       if (is_pts) for_tm_half(tp, dist);
-      const float d0 = group_rs8(dq, g), d1 = group_rs8(dq + KR, g);
+      const float d0 = group_rs8(dq), d1 = group_rs8(dq + KR);
       const float mine = (real_me[0] ? w_me[0] * sqrtf(d0) : 0.0f) +
                          (real_me[1] ? w_me[1] * sqrtf(d1) : 0.0f);
       const float obj = block_sum0(mine, scal, warp, lane);
@@ -669,6 +706,7 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
       }
     }
   }
+  cp_wait_all();
   tm::dealloc_cta<TM_COLS>(tbase, warp);
 }
 
@@ -689,6 +727,8 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
                  float tol, float* x_out, float* obj_out, int* iters_out, float* tr_obj,
                  FailureSlot* fail, unsigned long long* invalid) {
   extern __shared__ __align__(16) float smem[];
+  float* const stage = smem + SM_STAGE;
+  float* const wst = smem + SM_WST;
   float* const red = smem + SM_RED;
   float* const cb = smem + SM_CB;  // x of the coming pass
   int* const ctl = reinterpret_cast<int*>(smem + SM_GR);
@@ -706,7 +746,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   bool real_me[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    k_me[h] = 2 * ((KR * h + (g >> 1)) * NG + gid) + (g & 1);
+    k_me[h] = pair_point0(KR * h, g, gid);  // register slot 0 = point slot g
     real_me[h] = is_pts && k_me[h] < n;
   }
   const int cgrp = lane >> 2, cidx = 2 * (lane & 3);
@@ -714,19 +754,30 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   const bool cv0 = cgrp < 7, cv1 = cgrp < 7 && (lane & 3) != 3;
   const int nd = n * D;
 
-  for (int64_t b = blockIdx.x; b < batch; b += gridDim.x) {
-    const float* const src = points + b * nd;
-    const float* const wsrc = weights + b * n;
+  int64_t b = blockIdx.x;
+  if (b < batch) {
+    stage_copy(stage, points + b * nd, nd);
+    stage_copy(wst, weights + b * n, n);
+  }
+  cp_commit();
+  for (; b < batch; b += gridDim.x) {
+    cp_wait_all();
+    __syncthreads();
+    const float* const src = stage + stage_shift(points + b * nd);
+    const float* const wsrc = wst + stage_shift(weights + b * n);
     float2 A[KR][J];
     float2 wq[KP];
     const Loaded ld = load_problem(src, wsrc, n, gid, g, is_pts, A, wq, tp);
     float w_me[2];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? __ldg(wsrc + k_me[h]) : 0.0f;
+    for (int h = 0; h < 2; ++h) w_me[h] = real_me[h] ? wsrc[k_me[h]] : 0.0f;
     check_problem(ld.bad_pt, wq, b, invalid);
-    __syncthreads();  // every warp is past the previous problem's ctl / row reads
-    if (b + gridDim.x < batch)
-      prefetch_problem(points + (b + gridDim.x) * nd, weights + (b + gridDim.x) * n, nd, n);
+    __syncthreads();  // every thread is done with the stage
+    if (b + gridDim.x < batch) {  // the next problem streams in during this one's passes
+      stage_copy(stage, points + (b + gridDim.x) * nd, nd);
+      stage_copy(wst, weights + (b + gridDim.x) * n, n);
+    }
+    cp_commit();
 
     // ---- x_0: x_init, or the weighted mean points * (w / sum w) (irls.hpp:32, types.hpp:73)
     if (x_init == nullptr) weighted_sum_rows(A, tp, wq, myrow, is_pts, lane);
@@ -765,7 +816,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
 #pragma unroll
           for (int m = 0; m < KR; ++m) dist(m, i, A[m][i]);
         for_tm_half(tp, dist);
-        float d2[2] = {group_rs8(dq, g), group_rs8(dq + KR, g)};
+        float d2[2] = {group_rs8(dq), group_rs8(dq + KR)};
         // irls.hpp:45-46 and costs.hpp:24-33 / :13-20 with one hardware reciprocal square root
         // per point each (rsqrt.approx: ~2 ulp, against an FP64 reference)
         float beta[2], sur = 0.0f, cost = 0.0f;
@@ -783,8 +834,8 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
 #pragma unroll
           for (int i = 0; i < J; ++i) acc[i] = make_float2(0.0f, 0.0f);
           float2 bq[KP];
-          group_ag8(beta[0], bq, lane);
-          group_ag8(beta[1], bq + KR, lane);
+          group_ag8(beta[0], bq);
+          group_ag8(beta[1], bq + KR);
 #pragma unroll
           for (int m = 0; m < KR; ++m)
 #pragma unroll
@@ -860,6 +911,7 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
       }
     }
   }
+  cp_wait_all();
   tm::dealloc_cta<TM_COLS>(tbase, warp);
 }
 
