@@ -52,6 +52,7 @@ _VARIANT_TOKENS = {
     "cpt2": "-DNLEM_XW4_CPT=2",
     "cpt4": "-DNLEM_XW4_CPT=4",
     "cpt8": "-DNLEM_XW4_CPT=8",
+    "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-phase clock64 sums (printf)
 }
 
 
