@@ -36,13 +36,16 @@
 //  * the 54 per-lane partials (49 coordinates, sum ga, 4 history sums) are reduced with a
 //    shared-memory transpose (fixed tree: bitwise deterministic), the 49 consensus coordinates
 //    are finished by their owner lanes, which keep z, m and the c~ history in shared memory;
-//    the Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce.
+//    the Gram row <c~_{t-r}, c~_{t+1}> is a 6-value butterfly all-reduce kept in registers;
+//  * the point state of pair i + 1 is requested from TMEM (tcgen05.ld) before the arithmetic of
+//    pair i, the previous sweep's stores are waited for only there.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <utility>
 
 #include "launch.h"
+#include "tmem.cuh"
 
 namespace nlemk {
 
@@ -91,8 +94,7 @@ constexpr int W_RED = TILE;  // single tile buffer
 constexpr int W_CB = W_RED + 32 * RED_STR;
 constexpr int W_OWN = W_CB + KS * CB_STR;        // [4 + 2 (R+1)][32] owner scalars
 constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 ring
-constexpr int W_GR = W_NR + 8;  // [8] Gram row of the coming sweep: G[0..R-1], ||c~||^2, <m, c~>, ||c~_{t+1-R}||^2
-constexpr int W_TOTAL = W_GR + 8;
+constexpr int W_TOTAL = W_NR + 8;
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
 constexpr int kProbe = 1024;  // pixels sampled by the small-mu probe launch
 constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
@@ -331,7 +333,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   float* const W = smem + warp * W_TOTAL;
   float* const red = W + W_RED;
   float* const cb = W + W_CB;
-  float* const gram = W + W_GR;
   float* const own = W + W_OWN + lane;  // owner scalars, row stride 32 (lane-private column)
   float* const nrs = W + W_NR;          // ||c~||^2 history ring (warp-uniform)
 
@@ -415,6 +416,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #ifdef NLEM_LR_STAMPS
   long long st_t0 = 0, st_t1 = 0, st_t2 = 0, st_t3 = 0, st_wait = 0, st_setup = 0, st_sw = 0, st_epi = 0, st_n = 0;
   long long st_p[4] = {0, 0, 0, 0};
+  long long st_s[4] = {0, 0, 0, 0}, st_sq = 0;  // sweep phases: dot, update, patch sum, consensus
 #endif
   while (idx < nidx) {
     int nxt = 0;
@@ -585,31 +587,32 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     { const long long q_ = clock64(); st_p[3] += q_ - st_q; st_q = q_; }
 #endif
     int head = 0;
-    // publish c~ (owners' ring head) and the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep
-    auto publish = [&]() {
-      const float* hA = own + 4 * 32;
-      const float* hB = own + (4 + R + 1) * 32;
-      const float cA = hA[head * 32], cB = hB[head * 32];
-      const float mA = own[2 * 32], mB = own[3 * 32];
+    // Publish c~_{t+1} and form the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep.  The row
+    // stays in registers (every lane holds the butterfly result) and the owners pass c~_{t+1}, m
+    // and the four history vectors they already loaded for the consensus, so only c~ itself goes
+    // through shared memory (one __syncwarp): the consensus -> Gram -> dot-product hand-over is a
+    // serial chain that no other work of the warp overlaps, so every shared-memory round trip
+    // removed from it is time (34.0 vs 32.75 Mpix/s with the prefetched point state).
+    // gq = G_0..G_3, ||c~||^2, <m, c~>, ||c~_{t+1-R}||^2.
+    float gq[R + 3];
+    auto publish_regs = [&](float cA, float cB, float mA, float mB, const float (&hqA)[R],
+                            const float (&hqB)[R]) {
+      const float nrR = nrs[(head + 1) % (R + 1)];  // written R sweeps ago (0 while filling)
       float part[R + 2];
 #pragma unroll
-      for (int q = 0; q < R; ++q) {
-        const int sl = (head + R - q) % (R + 1);  // c~_{t-q} relative to the new head t+1
-        part[q] = fmaf(hA[sl * 32], cA, hB[sl * 32] * cB);
-      }
+      for (int q = 0; q < R; ++q) part[q] = fmaf(hqA[q], cA, hqB[q] * cB);
       part[R] = fmaf(cA, cA, cB * cB);
       part[R + 1] = fmaf(mA, cA, mB * cB);
+      if (own0) cb[jx0 * CB_STR + jy0] = cA;
+      if (own1) cb[jx1 * CB_STR + jy0] = cB;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
         for (int q = 0; q < R + 2; ++q) part[q] += __shfl_xor_sync(0xffffffffu, part[q], o);
 #pragma unroll
-      for (int q = 0; q < R + 2; ++q) gram[q] = part[q];  // same value in every lane
+      for (int q = 0; q < R + 2; ++q) gq[q] = part[q];  // same value in every lane
+      gq[R + 2] = nrR;
       if (lane == 0) nrs[head] = part[R];
-      if (own0) cb[jx0 * CB_STR + jy0] = cA;
-      if (own1) cb[jx1 * CB_STR + jy0] = cB;
-      __syncwarp();
-      if (lane == 0) gram[R + 2] = nrs[(head + 1) % (R + 1)];  // ||c~_{t+1-R}||^2 (0 while filling)
       __syncwarp();
     };
     tm_wait_st();
@@ -689,7 +692,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       // the minimiser is x at the stop pass (or x_T), held in own[0/32]
       if (ifail_iter < 0) iters = stop_at > 0 ? stop_at : P.iters;
     } else {
-    publish();
+    {
+      const float zero4[R] = {0.0f, 0.0f, 0.0f, 0.0f};
+      __syncwarp();  // the owners' initial rows (and the cleared norm ring) are visible
+      publish_regs(own[4 * 32], own[(4 + R + 1) * 32], own[2 * 32], own[3 * 32], zero4, zero4);
+    }
 #ifdef NLEM_LR_STAMPS
     st_t2 = clock64(); st_setup += st_t2 - st_t1;
 #endif
@@ -697,8 +704,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // when the self point's prox scale saturates at sweep 1 (lambda_self = 1/mu >= ||z_0 - a_self||
     // = ||c~_1||), most scales do, no history term decays and the ring would overflow after R
     // sweeps - the pixel goes to the exact kernel right away.  A heuristic: a wrong guess costs
-    // time, never accuracy.  Warp-uniform (gram[] holds the same value in every lane).
-    if (P.iters > R && !static_eq && inv_mu * inv_mu >= gram[R]) ovf = true;
+    // time, never accuracy.  Warp-uniform (gq[] holds the same value in every lane).
+    if (P.iters > R && !static_eq && inv_mu * inv_mu >= gq[R]) ovf = true;
     for (int t = 1; t <= P.iters && !ovf && !probe_n; ++t) {
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
@@ -707,6 +714,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       float usum = 0.0f;
       bool fnorm = false, sne1 = false;
       float2 Dk2[SEGL];
+#ifdef NLEM_LR_STAMPS
+      st_sq = clock64();
+#endif
       {
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) Dk2[i] = make_float2(0.0f, 0.0f);
@@ -724,13 +734,16 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           p_dot(Dk2, v, cvx);
         }
       }
+#ifdef NLEM_LR_STAMPS
+      { const long long q_ = clock64(); st_s[0] += q_ - st_sq; st_sq = q_; }
+#endif
       {
         float lm[16];
         tm_ld16c_wait<2 * NF * SEGL>(tw, lm);
         float G[R];
 #pragma unroll
-        for (int q = 0; q < R; ++q) G[q] = gram[q];
-        const float Gnn = gram[R], Cm = gram[R + 1], nrR = gram[R + 2];
+        for (int q = 0; q < R; ++q) G[q] = gq[q];
+        const float Gnn = gq[R], Cm = gq[R + 1], nrR = gq[R + 2];
         float2 vac2[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) vac2[q] = make_float2(0.0f, 0.0f);
@@ -742,11 +755,18 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         // = 1/mu != 0) non-finite in the same sweep, so the flagged sweep is the reference's.
         float2 nchk = make_float2(0.0f, 0.0f);
         float hmax = -1.0f;
+        // the state of point pair i + 1 is requested before the arithmetic of pair i
+        uint32_t stq[2][16];
+        tm_wait_st();  // the previous sweep's state stores (they had three phases to land)
+        tm::ld16_issue<0>(tw, stq[0]);
         static_for<SEGL>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           // point i of both slots as one register pair per field
           float st[16];
-          tm_ld16c_wait<i * 2 * NF>(tw, st);
+          tm::wait_ld(stq[i & 1]);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) st[q] = __uint_as_float(stq[i & 1][q]);
+          if constexpr (i + 1 < SEGL) tm::ld16_issue<(i + 1) * 2 * NF>(tw, stq[(i + 1) & 1]);
           const float2 H = make_float2(st[0], st[1]), K = make_float2(st[2], st[3]);
           const float2 ga = make_float2(st[4], st[5]), a2 = make_float2(st[6], st[7]);
           const float2 al0 = make_float2(st[8], st[9]), al1 = make_float2(st[10], st[11]);
@@ -795,7 +815,6 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           vac2[3] = __fadd2_rn(vac2[3], o3);
           u[i] = oga;
           us2 = __fadd2_rn(us2, oga);
-          // column pairs per store (x8 / x16 register tuples fragment the register file: spills)
 #if NLEM_LR_ST == 4
           static_for<4>([&](auto qc) {
             constexpr int q = decltype(qc)::value;
@@ -834,38 +853,54 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       // a ring overflow / cancellation hands the whole pixel to the exact kernel: stop now
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
       float gA, gB, xs[5];
+#ifdef NLEM_LR_STAMPS
+      { const long long q_ = clock64(); st_s[1] += q_ - st_sq; st_sq = q_; }
+#endif
       {
         const float ex[5] = {usum, vac[0], vac[1], vac[2], vac[3]};
         patch_sum_reduce(u, ex, gA, gB, xs);
       }
+#ifdef NLEM_LR_STAMPS
+      { const long long q_ = clock64(); st_s[2] += q_ - st_sq; st_sq = q_; }
+#endif
       // (4) consensus z' = P_C(z - g/n), c = 2 z' - z  (admm.hpp:59-65 in p-form);
       // g_j = sum_q v_q c~_{t-q, j} - (sum_k ga'_k a_kj - U m_j)
       bool zbad = false, zne = false;
       const int nhead = (head + 1) % (R + 1);
+      // every lane loads its (lane-private) owner column - zeros outside the owners - once: the
+      // history vectors serve the consensus and then the Gram row of the next sweep
+      float hq[2][R], cn[2], mr[2];
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        if (hf ? own1 : own0) {
-          float* h = own + (4 + hf * (R + 1)) * 32;
-          const float z = own[hf * 32], m = own[(2 + hf) * 32];
-          float g = 0.0f;
+        float* h = own + (4 + hf * (R + 1)) * 32;
+        const float z = own[hf * 32];
+        mr[hf] = own[(2 + hf) * 32];
 #pragma unroll
-          for (int q = R - 1; q >= 0; --q) g = fmaf(xs[1 + q], h[((head + R + 1 - q) % (R + 1)) * 32], g);
-          g -= fmaf(-xs[0], m, hf ? gB : gA);
-          const float zn = box_clamp(fmaf(-g, inv_n, z), P.range);
+        for (int q = 0; q < R; ++q) hq[hf][q] = h[((head + R + 1 - q) % (R + 1)) * 32];
+        float g = 0.0f;
+#pragma unroll
+        for (int q = R - 1; q >= 0; --q) g = fmaf(xs[1 + q], hq[hf][q], g);
+        g -= fmaf(-xs[0], mr[hf], hf ? gB : gA);
+        const float zn = box_clamp(fmaf(-g, inv_n, z), P.range);
+        cn[hf] = 0.0f;
+        if (hf ? own1 : own0) {
           zbad |= !isfinite(zn);
           zne |= zn != a0;
           if (hf == 0 && frames != nullptr && lane == kCenterLane)
             frames[static_cast<int64_t>(t - 1) * plane + pix] = zn;
           own[hf * 32] = zn;
-          h[nhead * 32] = (2.0f * zn - z) - m;
+          cn[hf] = (2.0f * zn - z) - mr[hf];
+          h[nhead * 32] = cn[hf];
         }
       }
-      const unsigned bad_z = __ballot_sync(0xffffffffu, zbad), bad_n = __ballot_sync(0xffffffffu, fnorm);
-      const unsigned bad_o = __ballot_sync(0xffffffffu, ovf);
-      if (bad_z | bad_n | bad_o) {
+      // one vote for the rare events; the separate ballots only when one fired
+      if (__any_sync(0xffffffffu, zbad | fnorm | ovf)) {
+        const unsigned bad_z = __ballot_sync(0xffffffffu, zbad), bad_n = __ballot_sync(0xffffffffu, fnorm);
+        const unsigned bad_o = __ballot_sync(0xffffffffu, ovf);
         // a hand-off (ring overflow / cancellation) outranks a failure: the exact kernel redoes
         // the whole pixel and records any failure itself
         if (!bad_o) fw = bad_z ? 2 * t : 2 * t + 1;
+        ovf = bad_o != 0u;
         break;
       }
       if (static_eq && !__any_sync(0xffffffffu, sne1 | zne)) {  // residual exactly 0
@@ -874,9 +909,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       }
       if (t < P.iters) {
         head = nhead;
-        tm_wait_st();
-        publish();
+        publish_regs(cn[0], cn[1], mr[0], mr[1], hq[0], hq[1]);
       }
+#ifdef NLEM_LR_STAMPS
+      { const long long q_ = clock64(); st_s[3] += q_ - st_sq; st_sq = q_; }
+#endif
     }
     }  // ADMM
     tm_wait_st();
@@ -917,8 +954,10 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     printf("lr stamps blk %d warp %d: pixels %lld tile_wait %lld setup %lld sweeps %lld epilogue %lld (cycles/pixel)\n",
            blockIdx.x, warp, st_n, st_wait / st_n, st_setup / st_n, st_sw / st_n, st_epi / st_n);
   if (blockIdx.x < 2 && lane == 0 && warp == 0 && st_n)
-    printf("lr setup: footprint %lld distances+weights+tmem %lld nlm-init(patch sum) %lld owners %lld\n",
-           st_p[0] / st_n, st_p[1] / st_n, st_p[2] / st_n, st_p[3] / st_n);
+    printf("lr setup: footprint %lld distances+weights+tmem %lld nlm-init(patch sum) %lld owners %lld\n"
+           "lr sweeps (all T, cycles/pixel): dot %lld update %lld patch-sum+reduce %lld consensus+publish %lld\n",
+           st_p[0] / st_n, st_p[1] / st_n, st_p[2] / st_n, st_p[3] / st_n, st_s[0] / st_n, st_s[1] / st_n,
+           st_s[2] / st_n, st_s[3] / st_n);
 #endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
