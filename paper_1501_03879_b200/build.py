@@ -53,6 +53,8 @@ _VARIANT_TOKENS = {
     "cpt4": "-DNLEM_XW4_CPT=4",
     "cpt8": "-DNLEM_XW4_CPT=8",
     "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-phase clock64 sums (printf)
+    "lrw4": "-DNLEM_LR_WARPS=4",     # image low-rank kernel: 4 pixel-warps per SM (unloaded phase latencies)
+    "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-phase clock64 sums (printf)
 }
 
 

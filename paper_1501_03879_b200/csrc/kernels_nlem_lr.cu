@@ -369,6 +369,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const int jy0 = lane % KS, jx0 = lane / KS, jx1 = 4 + lane / KS;
 
   const float inv_mu = 1.0f / P.mu;
+  // box as a pair of bounds (infinite when unconstrained): the clamp is two selects
+  const float box_lo = P.range.bounded ? P.range.lower : -__int_as_float(0x7f800000);
+  const float box_hi = P.range.bounded ? P.range.upper : __int_as_float(0x7f800000);
   const bool nlm_init = P.init_mode == NLEM_INIT_NLM_PATCH;
   const bool irls = P.solver == NLEM_SOLVER_IRLS;
   const int total_warps = gridDim.x * WARPS;
@@ -417,6 +420,12 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   long long st_t0 = 0, st_t1 = 0, st_t2 = 0, st_t3 = 0, st_wait = 0, st_setup = 0, st_sw = 0, st_epi = 0, st_n = 0;
   long long st_p[4] = {0, 0, 0, 0};
   long long st_s[4] = {0, 0, 0, 0}, st_sq = 0;  // sweep phases: dot, update, patch sum, consensus
+  long long st_f[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, st_fq = 0;  // fine stamps
+#define LR_FSTAMP(k) { const long long q_ = clock64(); st_f[k] += q_ - st_fq; st_fq = q_; }
+#define LR_FSTART() { st_fq = clock64(); }
+#else
+#define LR_FSTAMP(k)
+#define LR_FSTART()
 #endif
   while (idx < nidx) {
     int nxt = 0;
@@ -516,6 +525,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // Half A rows (jx - 0) * 7 + jy, half B rows (jx - 4) * 7 + jy, then 5 extra scalars.
     auto patch_sum_reduce = [&](const float2 (&u2)[SEGL], const float (&extra)[5], float& oA,
                                 float& oB, float (&xs)[5]) {
+      LR_FSTART()
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
         const int jxa = hf ? 4 : 0, jxb = hf ? KS : 4;
@@ -535,10 +545,14 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
           for (int q = 0; q < 5; ++q) red[(3 * KS + q) * RED_STR + lane] = extra[q];
         }
+        LR_FSTAMP(hf ? 3 : 0)
         __syncwarp();
-        float rr = 0.0f;
-        if (lane < (hf ? 3 * KS + 5 : 4 * KS)) rr = row_sum(red + lane * RED_STR);
+        LR_FSTAMP(hf ? 4 : 1)
+        // every lane sums its row (rows beyond the half's count hold stale, unused values:
+        // every consumer is masked by the owner predicates) - no divergent branch
+        const float rr = row_sum(red + lane * RED_STR);
         __syncwarp();
+        LR_FSTAMP(hf ? 5 : 2)
         if (hf == 0) {
           oA = rr;
         } else {
@@ -586,7 +600,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #ifdef NLEM_LR_STAMPS
     { const long long q_ = clock64(); st_p[3] += q_ - st_q; st_q = q_; }
 #endif
-    int head = 0;
+    // ring slots: sl[q] holds c~_{t-q} (q < R), sl[R] is the free slot; rotated once per sweep
+    int sl[R + 1] = {0, 4, 3, 2, 1};
     // Publish c~_{t+1} and form the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep.  The row
     // stays in registers (every lane holds the butterfly result) and the owners pass c~_{t+1}, m
     // and the four history vectors they already loaded for the consensus, so only c~ itself goes
@@ -597,7 +612,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     float gq[R + 3];
     auto publish_regs = [&](float cA, float cB, float mA, float mB, const float (&hqA)[R],
                             const float (&hqB)[R]) {
-      const float nrR = nrs[(head + 1) % (R + 1)];  // written R sweeps ago (0 while filling)
+      const float nrR = nrs[sl[R]];  // ||c~_{t+1-R}||^2, written R sweeps ago (0 while filling)
       float part[R + 2];
 #pragma unroll
       for (int q = 0; q < R; ++q) part[q] = fmaf(hqA[q], cA, hqB[q] * cB);
@@ -612,7 +627,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #pragma unroll
       for (int q = 0; q < R + 2; ++q) gq[q] = part[q];  // same value in every lane
       gq[R + 2] = nrR;
-      if (lane == 0) nrs[head] = part[R];
+      if (lane == 0) nrs[sl[0]] = part[R];
       __syncwarp();
     };
     tm_wait_st();
@@ -823,7 +838,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #elif NLEM_LR_ST == 2
           static_for<8>([&](auto qc) {
             constexpr int q = decltype(qc)::value;
-            tm_st2c<i * 2 * NF + 2 * q>(tw, o[2 * q], o[2 * q + 1]);
+            if constexpr (q != 3)  // field 3 (||a~||^2) never changes: not rewritten
+              tm_st2c<i * 2 * NF + 2 * q>(tw, o[2 * q], o[2 * q + 1]);
           });
 #else
           static_for<16>([&](auto qc) {
@@ -865,34 +881,46 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #endif
       // (4) consensus z' = P_C(z - g/n), c = 2 z' - z  (admm.hpp:59-65 in p-form);
       // g_j = sum_q v_q c~_{t-q, j} - (sum_k ga'_k a_kj - U m_j)
-      bool zbad = false, zne = false;
-      const int nhead = (head + 1) % (R + 1);
-      // every lane loads its (lane-private) owner column - zeros outside the owners - once: the
-      // history vectors serve the consensus and then the Gram row of the next sweep
-      float hq[2][R], cn[2], mr[2];
+      // Every lane loads its (lane-private) owner column - zeros outside the owners - in one
+      // batch: z, m and the four history vectors of both halves, which serve the consensus and
+      // then the Gram row of the next sweep.  All loads precede all stores (the compiler cannot
+      // tell the rows apart and would otherwise serialise the two halves), and the arithmetic is
+      // branch-free, so the two halves' dependency chains interleave.
+      const int nslot = sl[R];  // the free ring slot receives c~_{t+1}
+      float hq[2][R], zr[2], mr[2], zn[2], cn[2];
+      zr[0] = own[0];
+      zr[1] = own[32];
+      mr[0] = own[2 * 32];
+      mr[1] = own[3 * 32];
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        hq[0][q] = own[(4 + sl[q]) * 32];
+        hq[1][q] = own[(4 + R + 1 + sl[q]) * 32];
+      }
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
-        float* h = own + (4 + hf * (R + 1)) * 32;
-        const float z = own[hf * 32];
-        mr[hf] = own[(2 + hf) * 32];
-#pragma unroll
-        for (int q = 0; q < R; ++q) hq[hf][q] = h[((head + R + 1 - q) % (R + 1)) * 32];
         float g = 0.0f;
 #pragma unroll
         for (int q = R - 1; q >= 0; --q) g = fmaf(xs[1 + q], hq[hf][q], g);
         g -= fmaf(-xs[0], mr[hf], hf ? gB : gA);
-        const float zn = box_clamp(fmaf(-g, inv_n, z), P.range);
-        cn[hf] = 0.0f;
-        if (hf ? own1 : own0) {
-          zbad |= !isfinite(zn);
-          zne |= zn != a0;
-          if (hf == 0 && frames != nullptr && lane == kCenterLane)
-            frames[static_cast<int64_t>(t - 1) * plane + pix] = zn;
-          own[hf * 32] = zn;
-          cn[hf] = (2.0f * zn - z) - mr[hf];
-          h[nhead * 32] = cn[hf];
-        }
+        const float v = fmaf(-g, inv_n, zr[hf]);
+        const float y = v < box_lo ? box_lo : v;  // prox.hpp:45-50 (NaN passes through)
+        zn[hf] = box_hi < y ? box_hi : y;
+        cn[hf] = (hf ? own1 : own0) ? (2.0f * zn[hf] - zr[hf]) - mr[hf] : 0.0f;
       }
+      const bool zbad = (own0 && !isfinite(zn[0])) || (own1 && !isfinite(zn[1]));
+      const bool zne = (own0 && zn[0] != a0) || (own1 && zn[1] != a0);
+      if (own0) {
+        own[0] = zn[0];
+        own[(4 + nslot) * 32] = cn[0];
+      }
+      if (own1) {
+        own[32] = zn[1];
+        own[(4 + R + 1 + nslot) * 32] = cn[1];
+      }
+      if (frames != nullptr && lane == kCenterLane)
+        frames[static_cast<int64_t>(t - 1) * plane + pix] = zn[0];
+      LR_FSTAMP(6)  // xs shuffles + consensus
       // one vote for the rare events; the separate ballots only when one fired
       if (__any_sync(0xffffffffu, zbad | fnorm | ovf)) {
         const unsigned bad_z = __ballot_sync(0xffffffffu, zbad), bad_n = __ballot_sync(0xffffffffu, fnorm);
@@ -907,10 +935,15 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         iters = t;
         break;
       }
+      LR_FSTAMP(7)  // votes
       if (t < P.iters) {
-        head = nhead;
+        // rotate the ring: the slot just written becomes c~_{t+1}
+#pragma unroll
+        for (int q = R; q > 0; --q) sl[q] = sl[q - 1];
+        sl[0] = nslot;
         publish_regs(cn[0], cn[1], mr[0], mr[1], hq[0], hq[1]);
       }
+      LR_FSTAMP(8)  // publish
 #ifdef NLEM_LR_STAMPS
       { const long long q_ = clock64(); st_s[3] += q_ - st_sq; st_sq = q_; }
 #endif
@@ -955,9 +988,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
            blockIdx.x, warp, st_n, st_wait / st_n, st_setup / st_n, st_sw / st_n, st_epi / st_n);
   if (blockIdx.x < 2 && lane == 0 && warp == 0 && st_n)
     printf("lr setup: footprint %lld distances+weights+tmem %lld nlm-init(patch sum) %lld owners %lld\n"
-           "lr sweeps (all T, cycles/pixel): dot %lld update %lld patch-sum+reduce %lld consensus+publish %lld\n",
+           "lr sweeps (all T, cycles/pixel): dot %lld update %lld patch-sum+reduce %lld consensus+publish %lld\n"
+           "lr fine: macA %lld syncA %lld rowsumA %lld macB %lld syncB %lld rowsumB %lld consensus %lld votes %lld publish %lld\n",
            st_p[0] / st_n, st_p[1] / st_n, st_p[2] / st_n, st_p[3] / st_n, st_s[0] / st_n, st_s[1] / st_n,
-           st_s[2] / st_n, st_s[3] / st_n);
+           st_s[2] / st_n, st_s[3] / st_n, st_f[0] / st_n, st_f[1] / st_n, st_f[2] / st_n, st_f[3] / st_n,
+           st_f[4] / st_n, st_f[5] / st_n, st_f[6] / st_n, st_f[7] / st_n, st_f[8] / st_n);
 #endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
