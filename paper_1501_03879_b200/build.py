@@ -54,7 +54,6 @@ _VARIANT_TOKENS = {
     "cpt8": "-DNLEM_XW4_CPT=8",
     "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-phase clock64 sums (printf)
     "lrw4": "-DNLEM_LR_WARPS=4",     # image low-rank kernel: 4 pixel-warps per SM (unloaded phase latencies)
-    "lrst": "-DNLEM_LR_STAMPS",      # image low-rank kernel: per-phase clock64 sums (printf)
 }
 
 
