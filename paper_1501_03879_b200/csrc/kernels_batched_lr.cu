@@ -248,7 +248,18 @@ __device__ __forceinline__ void group_ag8(float mine, float2* out) {
 // Sum the 7 per-lane column partials over the 4 groups of the warp (lanes of group 0 then
 // hold the warp totals of their coordinates) and write them, with v7 in column 8 g + 7, as the
 // warp's partial row (two 16-byte stores per lane of group 0).
+// GROUP_ROWS (the IRLS kernel): no fold - `row` is the lane's GROUP row and every lane stores its
+// 7 column partials and v7; the consensus warp then sums NG rows in a tree whose first two levels
+// are exactly the fold's (bitwise the same sums; 17.26 vs 17.94 ms on config 1.  The ADMM kernel
+// keeps the fold: with group rows it measured 2.7 % slower, its consensus chain being longer).
+template <bool GROUP_ROWS = false>
 __device__ __forceinline__ void fold_store(float (&v)[J], float v7, float* row, int lane) {
+  if constexpr (GROUP_ROWS) {
+    float4* d = reinterpret_cast<float4*>(row + 8 * (lane & (G - 1)));
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v7);
+    return;
+  }
 #pragma unroll
   for (int o = G; o < 32; o <<= 1)
 #pragma unroll
@@ -259,15 +270,16 @@ __device__ __forceinline__ void fold_store(float (&v)[J], float v7, float* row, 
     d[1] = make_float4(v[4], v[5], v[6], v7);
   }
 }
-// Column pair (2 lane, 2 lane + 1) summed over the WARPS partial rows in a fixed tree.
+// Column pair (2 lane, 2 lane + 1) summed over the NR partial rows in a fixed tree.
+template <int NR = WARPS>
 __device__ __forceinline__ float2 rows_sum(const float* red, int lane) {
-  float2 r[WARPS];
+  float2 r[NR];
 #pragma unroll
-  for (int w = 0; w < WARPS; ++w) r[w] = reinterpret_cast<const float2*>(red + w * RS)[lane];
+  for (int w = 0; w < NR; ++w) r[w] = reinterpret_cast<const float2*>(red + w * RS)[lane];
 #pragma unroll
-  for (int span = 1; span < WARPS; span <<= 1)
+  for (int span = 1; span < NR; span <<= 1)
 #pragma unroll
-    for (int w = 0; w + span < WARPS; w += 2 * span) r[w] = __fadd2_rn(r[w], r[w + span]);
+    for (int w = 0; w + span < NR; w += 2 * span) r[w] = __fadd2_rn(r[w], r[w + span]);
   return r[0];
 }
 // columns 2 l, 2 l + 1 of a published row: the consensus lane l's pair.  SKEW (ADMM): columns
@@ -359,6 +371,7 @@ __device__ __forceinline__ void check_problem(bool bad_pt, const float2 (&wq)[KP
 // Weighted-mean numerator and denominator in one row pass (admm.hpp:40 / irls.hpp:32 with
 // types.hpp:71-74): the point warps write sum_k w_k a_k per coordinate and the weight sum (column
 // 7) into their partial rows; one barrier; the consensus warp divides (sum w a) / (sum w).
+template <bool GROUP_ROWS = false>
 __device__ __forceinline__ void weighted_sum_rows(const float2 (&A)[KR][J], uint32_t tp,
                                                   const float2 (&wq)[KP], float* myrow,
                                                   bool is_pts, int lane) {
@@ -377,21 +390,27 @@ __device__ __forceinline__ void weighted_sum_rows(const float2 (&A)[KR][J], uint
     float ws = 0.0f;  // weights of this lane's group (same in its 8 lanes), then of the warp
 #pragma unroll
     for (int m = 0; m < KP; ++m) ws += wq[m].x + wq[m].y;
-    ws += __shfl_xor_sync(0xffffffffu, ws, 8);
-    ws += __shfl_xor_sync(0xffffffffu, ws, 16);
-    fold_store(v, lane == 0 ? ws : 0.0f, myrow, lane);
+    if constexpr (GROUP_ROWS) {
+      fold_store<true>(v, (lane & (G - 1)) == 0 ? ws : 0.0f, myrow, lane);
+    } else {
+      ws += __shfl_xor_sync(0xffffffffu, ws, 8);
+      ws += __shfl_xor_sync(0xffffffffu, ws, 16);
+      fold_store(v, lane == 0 ? ws : 0.0f, myrow, lane);
+    }
   }
   __syncthreads();
 }
 
-// warp sums of four per-lane values (x0..x3) onto lanes r = lane & 3 (value x_r)
+// warp (or, GROUP_ROWS, 8-lane group) sums of four per-lane values (x0..x3) onto lanes
+// r = lane & 3 (value x_r)
+template <bool GROUP_ROWS = false>
 __device__ __forceinline__ float quad_sums(float x0, float x1, float x2, float x3, int lane) {
   const bool u2 = (lane & 2) != 0, u1 = (lane & 1) != 0;
   const float y0 = (u2 ? x2 : x0) + __shfl_xor_sync(0xffffffffu, u2 ? x0 : x2, 2);
   const float y1 = (u2 ? x3 : x1) + __shfl_xor_sync(0xffffffffu, u2 ? x1 : x3, 2);
   float hs = (u1 ? y1 : y0) + __shfl_xor_sync(0xffffffffu, u1 ? y0 : y1, 1);
 #pragma unroll
-  for (int o = 4; o < 32; o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
+  for (int o = 4; o < (GROUP_ROWS ? G : 32); o <<= 1) hs += __shfl_xor_sync(0xffffffffu, hs, o);
   return hs;
 }
 
@@ -721,6 +740,17 @@ admm_batched_lr(const float* __restrict__ points, const float* __restrict__ weig
 // and forms x_{p+1} = sum beta a / sum beta.  Failures are recorded as the generic kernel does
 // (iteration and kind of irls.hpp:39, :50, :52, :65-66).
 // ---------------------------------------------------------------------------------------
+namespace blr {
+// shared memory of the IRLS kernel (floats): stage and weights as above, then one partial row
+// per 8-lane group, x of the coming pass, the control word and the TMEM base
+constexpr int SI_CB = SM_RED + NG * RS;
+constexpr int SI_CTL = SI_CB + RSK;
+constexpr int SI_TB = SI_CTL + 4;
+constexpr int SI_TOTAL = SI_TB + 4;
+constexpr size_t SMEM_BYTES_IRLS = size_t(SI_TOTAL) * sizeof(float);
+static_assert(SI_CB % 4 == 0 && 2 * (SMEM_BYTES_IRLS + 1024) <= 233472, "two IRLS CTAs per SM");
+}  // namespace blr
+
 __global__ void __launch_bounds__(ALL, 2)
 irls_batched_reg(const float* __restrict__ points, const float* __restrict__ weights,
                  int64_t batch, int n, const float* __restrict__ x_init, float eps, int T,
@@ -729,9 +759,9 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   extern __shared__ __align__(16) float smem[];
   float* const stage = smem + SM_STAGE;
   float* const wst = smem + SM_WST;
-  float* const red = smem + SM_RED;
-  float* const cb = smem + SM_CB;  // x of the coming pass
-  int* const ctl = reinterpret_cast<int*>(smem + SM_GR);
+  float* const red = smem + SM_RED;  // [NG][RS]: one partial row per 8-lane group
+  float* const cb = smem + SI_CB;    // x of the coming pass
+  int* const ctl = reinterpret_cast<int*>(smem + SI_CTL);
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const int lane = tid & 31;
@@ -739,9 +769,9 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
   const int gid = warp * GPW + (lane >> 3);
   const bool is_pts = warp < WARPS;
   // TMEM: the second half of every lane's points (128 columns per CTA, two CTAs per SM)
-  const uint32_t tbase = tm::alloc_cta<TM_COLS>(reinterpret_cast<uint32_t*>(smem + SM_TB), warp);
+  const uint32_t tbase = tm::alloc_cta<TM_COLS>(reinterpret_cast<uint32_t*>(smem + SI_TB), warp);
   const uint32_t tp = tm::warp_addr(tbase, warp, (warp >> 2) * TM_WCOLS);
-  float* const myrow = red + (is_pts ? warp : 0) * RS;
+  float* const myrow = red + (is_pts ? gid : 0) * RS;
   int k_me[2];
   bool real_me[2];
 #pragma unroll
@@ -780,14 +810,14 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
     cp_commit();
 
     // ---- x_0: x_init, or the weighted mean points * (w / sum w) (irls.hpp:32, types.hpp:73)
-    if (x_init == nullptr) weighted_sum_rows(A, tp, wq, myrow, is_pts, lane);
+    if (x_init == nullptr) weighted_sum_rows<true>(A, tp, wq, myrow, is_pts, lane);
     float x0 = 0.0f, x1 = 0.0f;  // consensus warp: x of the current pass at cj, cj + 1
     if (warp == CW) {
       if (x_init != nullptr) {
         x0 = cv0 ? x_init[b * D + cj] : 0.0f;
         x1 = cv1 ? x_init[b * D + cj + 1] : 0.0f;
       } else {
-        const float2 s = rows_sum(red, lane);
+        const float2 s = rows_sum<NG>(red, lane);
         const float W = __shfl_sync(0xffffffffu, s.y, 3);  // sum of the weights (column 7)
         x0 = cv0 ? s.x / W : 0.0f;
         x1 = cv1 ? s.y / W : 0.0f;
@@ -845,12 +875,12 @@ irls_batched_reg(const float* __restrict__ points, const float* __restrict__ wei
           for (int i = 0; i < J; ++i) v[i] = acc[i].x + acc[i].y;
         }
         // warp sums of (beta, surrogate, cost, 0) onto lanes r = lane & 3
-        const float hs = quad_sums(beta[0] + beta[1], sur, cost, 0.0f, lane);
-        fold_store(v, lane < 4 ? hs : 0.0f, myrow, lane);
+        const float hs = quad_sums<true>(beta[0] + beta[1], sur, cost, 0.0f, lane);
+        fold_store<true>(v, g < 4 ? hs : 0.0f, myrow, lane);
       }
       __syncthreads();
       if (warp == CW) {
-        const float2 S = rows_sum(red, lane);
+        const float2 S = rows_sum<NG>(red, lane);
         const float den = __shfl_sync(0xffffffffu, S.y, 3);
         const float cur = __shfl_sync(0xffffffffu, S.y, 7);
         const float cst = __shfl_sync(0xffffffffu, S.y, 11);
@@ -930,13 +960,15 @@ bool irls_reg_supported(const IrlsLaunch& L) {
 cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream) {
   auto kfn = irls_batched_reg;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(SMEM_BYTES));
+                                       static_cast<int>(SMEM_BYTES_IRLS));
   if (e != cudaSuccess) return e;
   // shared-memory carve-out for kCtasPerSm resident CTAs (the rest of the 256 KB stays L1)
-  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, kCarveoutPct);
+  constexpr int carve =
+      static_cast<int>((kCtasPerSm * (SMEM_BYTES_IRLS + 1024) * 100 + 233471) / 233472) + 2;
+  e = cudaFuncSetAttribute(kfn, cudaFuncAttributePreferredSharedMemoryCarveout, carve);
   if (e != cudaSuccess) return e;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(L.batch, int64_t(kCtasPerSm) * device_caps().sms));
-  kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES, stream>>>(
+  kfn<<<static_cast<unsigned>(grid), ALL, SMEM_BYTES_IRLS, stream>>>(
       L.points, L.weights, L.batch, L.n, L.x_init, L.eps, L.max_iter, L.tol, L.x_out, L.obj_out,
       L.iters_out, L.tr_obj, L.fail, L.invalid);
   return cudaGetLastError();

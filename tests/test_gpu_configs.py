@@ -67,6 +67,31 @@ def test_config3_rows_vs_oracle(nb, oracle, config3):
     assert abs(_psnr(g, c) - _psnr(f, c)) <= PSNR_TOL
 
 
+def test_config3_reference_default_mu_rows_vs_oracle(nb, oracle):
+    """The benchmarked image at the reference's default penalty mu = 1e-3 (types.hpp:121), T = 10:
+    the small-mu probe routes the band to the exact p-form tile kernel.  A top band (clipped
+    windows), an interior band and a bottom band of the 4096-wide image, full width, against the
+    oracle on the same rows."""
+    import torch
+
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.config_image(3)
+    kw = dict(search=21, patch=7, h=synth.reference_h(30.0, 49), sigma=30.0, solver="admm",
+              solver_iters=10, mu=1e-3, init_mode="nlm")
+    p = nb.NlemParams(**kw)
+    o = oracle.make_params(**kw)
+    X = torch.from_numpy(noisy).cuda()
+    Xd = noisy.astype(np.float64)
+    worst = 0.0
+    for r0, r1 in ((0, 2), (2047, 2049), (4094, 4096)):
+        a0, a1 = max(0, r0 - 13), min(4096, r1 + 13)  # band + halo, global coordinates
+        g = nb.nlem_denoise_rows(X[a0:a1].contiguous(), a0, 4096, 4096, r0, r1 - r0, p).cpu().numpy()
+        f = oracle.nlem_denoise(Xd, o, rows=(r0, r1))[r0:r1]
+        worst = max(worst, float(np.abs(g.astype(np.float64) - f).max()))
+    assert worst <= TOL, worst
+
+
 def test_config3_whole_image_sanity(config3):
     """Every pixel finite and inside the box; denoising raises PSNR over the noisy input."""
     clean, noisy, out = config3
