@@ -1,4 +1,5 @@
-// Low-rank ("Gram-form") NLEM / EM-ADMM kernel for k = 7, S = 21 (configs 2, 3, 4).
+// Low-rank ("Gram-form") NLEM / EM-ADMM kernel for k = 7, S = 21 (configs 2, 3, 4); also the
+// IRLS comparator and the NlmOnly solver / nlm_denoise baseline in the same mapping.
 //
 // Algebra (p-form of admm.hpp:49-78).  With p_k = z - y_k/mu - a_k and
 // s_k = min(1, lambda_k / ||p_k||), one sweep is
@@ -374,6 +375,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const float box_hi = P.range.bounded ? P.range.upper : __int_as_float(0x7f800000);
   const bool nlm_init = P.init_mode == NLEM_INIT_NLM_PATCH;
   const bool irls = P.solver == NLEM_SOLVER_IRLS;
+  // NlmOnly (nlem.cpp:26-31, nlm.cpp:31-51): distances and weights as for NLEM, then only the
+  // centre coordinate of the weighted-mean patch - no point state, no sweeps
+  const bool nlm_only = P.solver == NLEM_SOLVER_NLM_ONLY;
   const int total_warps = gridDim.x * WARPS;
 
   // work items: pixels, or (probe launch) probe_n samples at pixel i * plane / probe_n
@@ -453,8 +457,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #endif
     // ---- footprint constancy (exact-stop candidate, admm.hpp:77 with tol 0)
     const float a0 = tile_at(T, gr0, gc0);
-    bool neq = false;
-    if (lane >= gc0 && lane <= gc1 + KS - 1) {
+    bool neq = nlm_only;  // NlmOnly never stops early: no footprint scan
+    if (!nlm_only && lane >= gc0 && lane <= gc1 + KS - 1) {
       // column `lane` of the footprint rows [gr0, gr1 + 6]: each column copy b (rows 7b..7b+12)
       // as four independent 16-byte loads (a rolled per-row loop of dependent 4-byte loads
       // cost ~4k cycles per pixel and warp)
@@ -508,6 +512,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         }
       }
       lm[14] = lm[15] = 0.0f;
+      if (!nlm_only) {
 #pragma unroll
       for (int i = 0; i < SEGL; ++i) {
         // H = ||a~||^2, K = -||a~||^2, ga = 0, ||a~||^2, al = 0 (slot-interleaved)
@@ -516,6 +521,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         tm_st<16>(t_pt(i), st);
       }
       tm_st<16>(t_lam(), lm);
+      }
     }
 #ifdef NLEM_LR_STAMPS
     { const long long q_ = clock64(); st_p[1] += q_ - st_q; st_q = q_; }
@@ -569,7 +575,25 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     // ---- initial patch (nlem.cpp:13-18): weighted mean (ratio form) or the noisy patch.
     // Owner scalars in shared memory: rows 0 z_A, 1 z_B, 2 m_A, 3 m_B, 4.. c~ history ring
     // (slot (head - q) mod (R+1) holds c~_{t-q}), A then B.
-    {
+    if (nlm_only) {
+      // sum_k w_k a_k[centre] / sum_k w_k (nlm.cpp:44): the centre coordinate (3, 3) of point i is
+      // row i + 3 of patch column 3; both sums through one butterfly (fixed order)
+      float2 v[14];
+      load_pcol(T + poff + (KS / 2) * PCS, v);
+      float2 cs2 = make_float2(0.0f, 0.0f), ws2 = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < SEGL; ++i) {
+        cs2 = __ffma2_rn(wgt[i], v[i + KS / 2], cs2);
+        ws2 = __fadd2_rn(ws2, wgt[i]);
+      }
+      float cs = cs2.x + cs2.y, ws = ws2.x + ws2.y;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        cs += __shfl_xor_sync(0xffffffffu, cs, o);
+        ws += __shfl_xor_sync(0xffffffffu, ws, o);
+      }
+      if (lane == kCenterLane) own[0] = box_clamp(cs / ws, P.range);  // clip_scalar / project_box
+    } else {
       const float mA = own0 ? tile_at(T, HS + jy0, HS + jx0) : 0.0f;
       const float mB = own1 ? tile_at(T, HS + jy0, HS + jx1) : 0.0f;
       float zA = mA, zB = mB;
@@ -635,7 +659,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     int fw = 0x7fffffff;  // first ADMM failure: 2 t (+1 for a non-finite norm)
     bool ovf = false;
     int ifail_iter = -1, ifail_kind = 0;  // IRLS failure record
-    if (irls) {
+    if (nlm_only) {
+      iters = 0;  // every frame holds the NLM value (nlem.cpp:28-30)
+    } else if (irls) {
       // ---- IRLS on the smooth surrogate (proj/include/nlem/irls.hpp:21-68).  Pass p evaluates
       // at x_p: the surrogate S(x_p) = sum w sqrt(||x_p - a||^2 + eps) and beta_k = w_k / sqrt(..),
       // then x_{p+1} = sum beta a / sum beta.  Pass 0 gives `previous`; pass t the iteration-t
@@ -1002,7 +1028,8 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 bool nlem_lr_supported(const NlemLaunch& L) {
   // 32-bit pixel indexing inside the kernel
   const int64_t lim = int64_t(1) << 30;
-  return (L.P.solver == NLEM_SOLVER_ADMM || L.P.solver == NLEM_SOLVER_IRLS) && L.P.patch == KS &&
+  return (L.P.solver == NLEM_SOLVER_ADMM || L.P.solver == NLEM_SOLVER_IRLS ||
+          L.P.solver == NLEM_SOLVER_NLM_ONLY) && L.P.patch == KS &&
          L.P.search == SW &&
          L.out_rows * L.cols < lim && L.rows < lim && L.pad_cols < lim;
 }
