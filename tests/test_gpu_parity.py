@@ -417,6 +417,28 @@ def test_lr_ring_handoff_small_mu(nb, oracle, tmp_path):
         assert (sum(handed) > 0) == expect_handoff, stats
 
 
+def test_reference_default_params_in_lr_kernel(nb, oracle, tmp_path):
+    """The reference's default NlemParams (nlem.hpp:23-35: S = 21, k = 7, 4 sweeps, mu = 1e-3, noisy
+    patch init) with h = 10 sigma as the reference CLI sets it (nlem_main.cpp:93).  With 4 sweeps
+    the history ring (R = 4) holds the whole history, so the low-rank kernel itself runs the
+    saturated regime (s_k = 1 for most points): frames and output vs the oracle, both inits,
+    and nothing handed to the exact kernel."""
+    from paper_1501_03879_b200 import synth
+
+    clean, noisy = synth.noisy_image(48, 72, 7, 5, 20.0)
+    for init in ("noisy", "nlm"):
+        g, o = _params_pair(nb, oracle, search=21, patch=7, h=10 * 20.0, iters=4, mu=1e-3, init=init)
+        fg = nb.nlem_denoise_snapshots(noisy, g)
+        _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
+        assert np.abs(fg - fo).max() <= TOL, init
+    stats = []
+    kw = dict(search=21, patch=7, h=10 * 20.0, solver="admm", solver_iters=4, mu=1e-3,
+              init_mode="noisy")
+    _run_forced_kernel("lr", noisy, kw, tmp_path, stats)
+    handed = [int(l.split(",")[1].split()[0]) for l in stats]
+    assert handed and sum(handed) == 0, stats
+
+
 def test_lr_kernel_matches_tile_kernel(nb, tmp_path):
     """The low-rank kernel (default for k=7/S=21 ADMM) and the exact p-form tile kernel agree
     on every frame of a config-3-parameter crop to FP32 rounding, and report the same
