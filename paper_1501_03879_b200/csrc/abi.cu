@@ -532,17 +532,34 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
     return invalid(failure, "input rows outside the image");
   if (out_rows == 0) return NLEM_OK;
   if (!noisy || !out) return invalid(failure, "null buffer");
-  // Mirror-padded band with a border of S/2 + k/2 on every side, so every patch of the
-  // full (unclipped) S x S window grid around each output pixel is addressable.
+  // The caller's band must cover the output rows and a halo of S/2 + k/2 rows (mirrored at the
+  // image edges): every patch of the S x S window grid around each output pixel.
   const int hb = params->search / 2 + params->patch / 2;
-  const int64_t pad_row0 = out_row0 - hb;
-  const int64_t pad_rows = out_rows + 2 * hb;
-  const int64_t pad_cols = cols + 2 * hb;
-  for (int64_t r = pad_row0; r < pad_row0 + pad_rows; ++r) {
+  for (int64_t r = out_row0 - hb; r < out_row0 + out_rows + hb; ++r) {
     const int64_t g = mirror_host(r, rows);
     if (g < in_row0 || g >= in_row0 + in_rows)
       return invalid(failure, "input rows do not cover the band and its halo");
   }
+  // Kernel choice: best specialised kernel for the shape; NLEM_KERNEL=lr|tile|fast|generic
+  // forces one (A/B measurements, tests; falls back to generic when unsupported).
+  enum class Kind { LR, TILE, FAST, GENERIC };
+  Kind kind = Kind::GENERIC;
+  {
+    NlemLaunch probe{nullptr, 0, 0, cols + 26, rows, cols, out_row0, out_rows,
+                     dev_params(*params), out, frames, nullptr};
+    const char* force = std::getenv("NLEM_KERNEL");  // per call: tests switch it in-process
+    const std::string k = force ? force : "";
+    if ((k.empty() || k == "lr") && nlem_lr_supported(probe)) kind = Kind::LR;
+    else if ((k.empty() || k == "tile") && nlem_tile_supported(probe)) kind = Kind::TILE;
+    else if ((k.empty() || k == "fast") && nlem_fast_supported(probe)) kind = Kind::FAST;
+  }
+  // Mirror-padded band.  The low-rank / tile kernels address a fixed (S_grid + k - 1)^2 tile per
+  // pixel and mask smaller windows inside their grid, so their border is the grid's; rows of
+  // that border beyond the caller's halo are read by zero-weight points only (clamped copies).
+  const int border = kind == Kind::LR || kind == Kind::TILE ? (params->patch == 7 ? 13 : 7) : hb;
+  const int64_t pad_row0 = out_row0 - border;
+  const int64_t pad_rows = out_rows + 2 * border;
+  const int64_t pad_cols = cols + 2 * border;
   if (failure) {  // image.hpp:16 over the rows this band reads
     DevSlot vs(s);
     cudaError_t e = vs.init();
@@ -558,17 +575,14 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
   DevSlot slot(s);
   e = slot.init();
   if (e == cudaSuccess)
-    e = launch_pad_band(noisy, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hb, s);
+    e = launch_pad_band(noisy, in_row0, in_rows, rows, cols, pad, pad_row0, pad_rows, pad_cols,
+                        border, s);
   if (e == cudaSuccess) {
     NlemDevParams dp = dev_params(*params);
     dp.nlm_ratio = nlm_ratio;
     NlemLaunch L{pad, pad_row0, pad_rows, pad_cols, rows, cols, out_row0, out_rows,
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
-    // kernel choice: best specialised kernel for the shape; NLEM_KERNEL=lr|tile|fast|generic
-    // forces one (A/B measurements; falls back to generic when unsupported)
-    const char* force = std::getenv("NLEM_KERNEL");  // per call: tests switch it in-process
-    const std::string k = force ? force : "";
-    if ((k.empty() || k == "lr") && nlem_lr_supported(L)) {
+    if (kind == Kind::LR) {
       // low-rank kernel, then the exact tile kernel over the pixels it handed off
       // [0] work counter, [1] hand-off count (-1: all), [2, 3] small-mu probe, [4..] hand-off list
       int* scratch = nullptr;
@@ -591,8 +605,8 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
         const cudaError_t ef = cudaFreeAsync(scratch, s);
         if (e == cudaSuccess) e = ef;
       }
-    } else if ((k.empty() || k == "tile") && nlem_tile_supported(L)) e = launch_nlem_tile(L, s);
-    else if ((k.empty() || k == "fast") && nlem_fast_supported(L)) e = launch_nlem_fast(L, s);
+    } else if (kind == Kind::TILE) e = launch_nlem_tile(L, s);
+    else if (kind == Kind::FAST) e = launch_nlem_fast(L, s);
     else e = launch_nlem_generic(L, s);
   }
   cudaFreeAsync(pad, s);

@@ -196,14 +196,18 @@ __device__ __forceinline__ int64_t mirror_index_dev(int64_t i, int64_t n) {
 
 // Mirror-padded band: pad[pr][pc] = image(mirror(pad_row0 + pr), mirror(pc - col_off)).
 // TMA has no mirror mode, so padding once keeps every later patch read in bounds.
-__global__ void pad_band_kernel(const float* __restrict__ in, int64_t in_row0, int64_t rows,
-                                int64_t cols, float* __restrict__ pad, int64_t pad_row0,
-                                int64_t pad_rows, int64_t pad_cols, int col_off) {
+// Rows outside the caller's band (only possible when a kernel's fixed tile border exceeds the
+// window's S/2 + k/2, i.e. a masked window smaller than the kernel's grid) are clamped to the
+// band: they are read by zero-weight grid points only and just have to be finite.
+__global__ void pad_band_kernel(const float* __restrict__ in, int64_t in_row0, int64_t in_rows,
+                                int64_t rows, int64_t cols, float* __restrict__ pad,
+                                int64_t pad_row0, int64_t pad_rows, int64_t pad_cols, int col_off) {
   const int64_t total = pad_rows * pad_cols;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t pr = i / pad_cols, pc = i - pr * pad_cols;
-    const int64_t gr = mirror_index_dev(pad_row0 + pr, rows);
+    int64_t gr = mirror_index_dev(pad_row0 + pr, rows);
+    gr = gr < in_row0 ? in_row0 : (gr >= in_row0 + in_rows ? in_row0 + in_rows - 1 : gr);
     const int64_t gc = mirror_index_dev(pc - col_off, cols);
     pad[i] = in[(gr - in_row0) * cols + gc];
   }
@@ -412,15 +416,15 @@ cudaError_t launch_irls_generic(const IrlsLaunch& L, cudaStream_t stream) {
   return err;
 }
 
-cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t rows, int64_t cols,
-                            float* pad, int64_t pad_row0, int64_t pad_rows, int64_t pad_cols, int hk,
-                            cudaStream_t stream) {
+cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t in_rows, int64_t rows,
+                            int64_t cols, float* pad, int64_t pad_row0, int64_t pad_rows,
+                            int64_t pad_cols, int hk, cudaStream_t stream) {
   const int64_t total = pad_rows * pad_cols;
   const int threads = 256;
   const int64_t blocks = std::min<int64_t>((total + threads - 1) / threads,
                                            static_cast<int64_t>(device_caps().sms) * 16);
   pad_band_kernel<<<static_cast<unsigned>(std::max<int64_t>(blocks, 1)), threads, 0, stream>>>(
-      in, in_row0, rows, cols, pad, pad_row0, pad_rows, pad_cols, hk);
+      in, in_row0, in_rows, rows, cols, pad, pad_row0, pad_rows, pad_cols, hk);
   return cudaGetLastError();
 }
 

@@ -370,6 +370,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   const int jy0 = lane % KS, jx0 = lane / KS, jx1 = 4 + lane / KS;
 
   const float inv_mu = 1.0f / P.mu;
+  const int hw = P.search >> 1, wlo = HS - hw;  // masked window for S < 21
   // box as a pair of bounds (infinite when unconstrained): the clamp is two selects
   const float box_lo = P.range.bounded ? P.range.lower : -__int_as_float(0x7f800000);
   const float box_hi = P.range.bounded ? P.range.upper : __int_as_float(0x7f800000);
@@ -446,10 +447,12 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     const float* const T = W;
 
     const int r = out_row0 + pix / cols, c = pix % cols;
-    const int gr0 = r < HS ? HS - r : 0;
-    const int gr1 = rows - 1 - r < HS ? HS + (rows - 1 - r) : SW - 1;
-    const int gc0 = c < HS ? HS - c : 0;
-    const int gc1 = cols - 1 - c < HS ? HS + (cols - 1 - c) : SW - 1;
+    // window of half-width hw = S/2 <= 10 inside the 21 x 21 grid, clipped at the image borders
+    // (patch.cpp:72-76); grid points outside it are zero-weight padding points
+    const int gr0 = r < hw ? HS - r : wlo;
+    const int gr1 = rows - 1 - r < hw ? HS + (rows - 1 - r) : SW - 1 - wlo;
+    const int gc0 = c < hw ? HS - c : wlo;
+    const int gc1 = cols - 1 - c < hw ? HS + (cols - 1 - c) : SW - 1 - wlo;
     const float inv_n = 1.0f / static_cast<float>((gr1 - gr0 + 1) * (gc1 - gc0 + 1));
 
 #ifdef NLEM_LR_STAMPS
@@ -1030,7 +1033,7 @@ bool nlem_lr_supported(const NlemLaunch& L) {
   const int64_t lim = int64_t(1) << 30;
   return (L.P.solver == NLEM_SOLVER_ADMM || L.P.solver == NLEM_SOLVER_IRLS ||
           L.P.solver == NLEM_SOLVER_NLM_ONLY) && L.P.patch == KS &&
-         L.P.search == SW &&
+         L.P.search <= SW &&  // smaller (odd) windows run masked inside the 21 x 21 grid
          L.out_rows * L.cols < lim && L.rows < lim && L.pad_cols < lim;
 }
 

@@ -393,6 +393,7 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
   __shared__ long long s_next_chunk[2];  // this CTA's next chunk (double-buffered)
   int chunk_parity = 0;
   constexpr int hs = C::SW / 2;
+  const int hw = P.search / 2, wlo = hs - hw;  // masked window (S <= SW)
   constexpr int center = C::D / 2;
   const int64_t plane = out_rows * cols;
   // list mode: only the listed band pixels (the low-rank kernel's hand-offs), in list order
@@ -430,10 +431,12 @@ nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, 
     for (int64_t q = ch * chunk; q < q_end; ++q) {
       const int64_t pix = pixel_at(q);
       const int64_t r = out_row0 + pix / cols, c = pix % cols;
-      const int gr0 = r < hs ? static_cast<int>(hs - r) : 0;
-      const int gr1 = rows - 1 - r < hs ? static_cast<int>(hs + (rows - 1 - r)) : C::SW - 1;
-      const int gc0w = c < hs ? static_cast<int>(hs - c) : 0;
-      const int gc1w = cols - 1 - c < hs ? static_cast<int>(hs + (cols - 1 - c)) : C::SW - 1;
+      // window of half-width hw = S/2 <= hs inside the kernel's SW x SW grid, clipped at the
+      // image borders (patch.cpp:72-76); grid points outside it are zero-weight padding
+      const int gr0 = r < hw ? static_cast<int>(hs - r) : wlo;
+      const int gr1 = rows - 1 - r < hw ? static_cast<int>(hs + (rows - 1 - r)) : C::SW - 1 - wlo;
+      const int gc0w = c < hw ? static_cast<int>(hs - c) : wlo;
+      const int gc1w = cols - 1 - c < hw ? static_cast<int>(hs + (cols - 1 - c)) : C::SW - 1 - wlo;
       const int n = (gr1 - gr0 + 1) * (gc1w - gc0w + 1);
       const float inv_n = 1.0f / static_cast<float>(n);
       // ---- tile (and its one-column-shifted copy) from the padded band; after the first
@@ -1093,8 +1096,10 @@ namespace nlemk {
 #endif
 
 bool nlem_tile_supported(const NlemLaunch& L) {
-  return (L.P.patch == 7 && L.P.search == 21) || (L.P.patch == 5 && L.P.search == 11);
+  // smaller (odd) windows run masked inside the kernel's grid
+  return (L.P.patch == 7 && L.P.search <= 21) || (L.P.patch == 5 && L.P.search <= 11);
 }
+
 
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream) {
   if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream);

@@ -69,7 +69,7 @@ struct NlemDevParams {
 };
 
 struct NlemLaunch {
-  const float* pad;  // mirror-padded band, row 0 = global row pad_row0, col 0 = global col -(S/2+k/2)
+  const float* pad;  // mirror-padded band, row 0 = global row pad_row0, col 0 = global col -border
   int64_t pad_row0, pad_rows, pad_cols;
   int64_t rows, cols;          // full image
   int64_t out_row0, out_rows;  // output band
@@ -86,9 +86,10 @@ cudaError_t launch_admm_generic(const AdmmLaunch& L, cudaStream_t stream, const 
 cudaError_t launch_collinear(const float* points, int64_t batch, int n, int d, int* list,
                              int* count, cudaStream_t stream);
 cudaError_t launch_irls_generic(const IrlsLaunch& L, cudaStream_t stream);
-cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t rows, int64_t cols,
-                            float* pad, int64_t pad_row0, int64_t pad_rows, int64_t pad_cols,
-                            int col_off, cudaStream_t stream);
+cudaError_t launch_pad_band(const float* in, int64_t in_row0, int64_t in_rows, int64_t rows,
+                            int64_t cols, float* pad, int64_t pad_row0, int64_t pad_rows,
+                            int64_t pad_cols, int col_off, cudaStream_t stream);
+
 cudaError_t launch_nlem_generic(const NlemLaunch& L, cudaStream_t stream);
 
 // Specialised register-tiled kernels (kernels_fast.cu).  Return false when the

@@ -1,8 +1,8 @@
 """GPU parity of the rows SURVEY §8 lists next to the solvers: nlm_denoise and the NlmOnly
 solver (proj/src/nlm.cpp:31-51, proj/src/nlem.cpp:26-31) on noisy inputs, the single-pixel
 drop-ins build_patch_stack / solve_patch (proj/src/patch.cpp:90-114, proj/src/nlem.cpp:20-56),
-and the exact p-form 'fast' image kernel (k=7 / k=5 at search windows the low-rank and tile
-kernels do not take).  Every comparison is against the FP64 oracle on the same float32
+and smaller search windows (k=7 with S < 21, k=5 with S < 11: masked inside the low-rank / tile
+kernels' grids by default, the exact p-form 'fast' image kernel when forced).  Every comparison is against the FP64 oracle on the same float32
 input.  Bar: 1e-2 gray levels (north_star)."""
 import math
 
@@ -153,13 +153,18 @@ def test_solve_patch_errors(nb):
         nb.solve_patch(st, p)
 
 
-# ------------------------------------------------------------------ the 'fast' image kernel
+# ------------------------------------------------- smaller search windows (k = 7 / k = 5)
 @pytest.mark.parametrize("k,S", [(7, 15), (7, 19), (5, 9), (5, 7)])
 @pytest.mark.parametrize("shape", [(33, 29), (6, 40)])
-def test_fast_kernel_shapes_vs_oracle(nb, oracle, k, S, shape):
-    """nlem_pixels_fast (exact p-form, patch stack in shared memory) serves k=7 / k=5 at the
-    search windows the low-rank (S=21) and tile (S=21 / 11) kernels do not; ragged images
-    (rows < S) included.  ADMM and NlmOnly, every frame vs the oracle."""
+@pytest.mark.parametrize("force", ["", "fast"])
+def test_small_window_shapes_vs_oracle(nb, oracle, monkeypatch, k, S, shape, force):
+    """k = 7 with S < 21 and k = 5 with S < 11.  Default dispatch: the low-rank / tile kernels run
+    the smaller window MASKED inside their fixed 21 x 21 / 11 x 11 grid (zero-weight points
+    outside it, a padded-band border of the grid's size).  NLEM_KERNEL=fast: nlem_pixels_fast
+    (exact p-form, patch stack in shared memory), the previous route for these shapes.  Ragged
+    images (rows < S) included.  ADMM and NlmOnly, every frame vs the oracle."""
+    if force:
+        monkeypatch.setenv("NLEM_KERNEL", force)  # read per call
     rng = np.random.default_rng(k * 100 + S)
     img = (rng.uniform(0, 255, shape) + rng.normal(0, 25, shape)).astype(np.float32)
     h = 25.0 * 10 * k
@@ -170,4 +175,37 @@ def test_fast_kernel_shapes_vs_oracle(nb, oracle, k, S, shape):
                                solver_iters=6, mu=1.0, init_mode="nlm")
         fg = nb.nlem_denoise_snapshots(img, g)
         _, fo = oracle.nlem_denoise(img.astype(np.float64), o, snapshots=True)
-        assert np.abs(fg - fo).max() <= TOL, (solver, k, S, shape)
+        assert np.abs(fg - fo).max() <= TOL, (solver, k, S, shape, force)
+
+
+@pytest.mark.parametrize("k,S", [(7, 7), (7, 11), (7, 13), (7, 17), (5, 5)])
+def test_masked_window_all_solvers_and_bands(nb, oracle, k, S):
+    """Masked windows through every solver of the low-rank / tile kernels (ADMM at mu = 1, ADMM at
+    mu = 1e-3 with 8 sweeps - the hand-off to the exact tile kernel -, IRLS, NlmOnly; noisy and
+    NLM init) vs the oracle, and a 3-band split with S/2 + k/2 halo rows (less than the kernels'
+    fixed tile border: the band padding clamps) bitwise equal to the whole-image call."""
+    import torch
+
+    rng = np.random.default_rng(1000 + 31 * k + S)
+    img = (rng.uniform(0, 255, (40, 37)) + rng.normal(0, 20, (40, 37))).astype(np.float32)
+    h = 20.0 * 10 * k
+    cases = [dict(solver="admm", mu=1.0, init_mode="nlm", solver_iters=6),
+             dict(solver="admm", mu=1e-3, init_mode="noisy", solver_iters=8),
+             dict(solver="irls", epsilon=1e-4, irls_tol=-1.0, init_mode="nlm", solver_iters=6),
+             dict(solver="nlm_only", init_mode="nlm", solver_iters=3)]
+    for kw in cases:
+        g = nb.NlemParams(search=S, patch=k, h=h, **kw)
+        okw = dict(kw, solver={"nlm_only": "nlm"}.get(kw["solver"], kw["solver"]))
+        o = oracle.make_params(search=S, patch=k, h=h, **okw)
+        fg = nb.nlem_denoise_snapshots(img, g)
+        _, fo = oracle.nlem_denoise(img.astype(np.float64), o, snapshots=True)
+        assert np.abs(fg - fo).max() <= TOL, (kw, k, S)
+    g = nb.NlemParams(search=S, patch=k, h=h, **cases[0])
+    X = torch.from_numpy(img).cuda()
+    whole = nb.nlem_denoise(X, g).cpu().numpy()
+    halo = S // 2 + k // 2
+    parts = []
+    for r0, r1 in ((0, 13), (13, 27), (27, 40)):
+        a0, a1 = max(0, r0 - halo), min(40, r1 + halo)
+        parts.append(nb.nlem_denoise_rows(X[a0:a1].contiguous(), a0, 40, 37, r0, r1 - r0, g).cpu().numpy())
+    assert np.array_equal(np.concatenate(parts), whole)
