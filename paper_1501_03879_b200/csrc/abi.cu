@@ -556,7 +556,12 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
   // Mirror-padded band.  The low-rank / tile kernels address a fixed (S_grid + k - 1)^2 tile per
   // pixel and mask smaller windows inside their grid, so their border is the grid's; rows of
   // that border beyond the caller's halo are read by zero-weight points only (clamped copies).
-  const int border = kind == Kind::LR || kind == Kind::TILE ? (params->patch == 7 ? 13 : 7) : hb;
+  int border = hb;
+  if (kind == Kind::LR || kind == Kind::TILE) {
+    NlemLaunch probe{nullptr, 0, 0, cols + 26, rows, cols, out_row0, out_rows,
+                     dev_params(*params), out, frames, nullptr};
+    border = nlem_tile_grid(probe) / 2 + params->patch / 2;
+  }
   const int64_t pad_row0 = out_row0 - border;
   const int64_t pad_rows = out_rows + 2 * border;
   const int64_t pad_cols = cols + 2 * border;

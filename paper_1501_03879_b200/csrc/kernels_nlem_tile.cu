@@ -114,6 +114,11 @@ struct TileCfg {
 // profiles/r1_tile_phase_times.txt; they are not part of the build.)
 using TileK7S21 = TileCfg<7, 21, 7, 4>;
 using TileK5S11 = TileCfg<5, 11, 11, 0>;   // config 0: 11 groups of 5 lanes, 2 warps
+// the remaining odd patch sides up to 7 with windows up to 21 (masked inside the grid when
+// smaller): the same template, so no shape with k <= 7 and S <= 21 falls to the generic kernel
+using TileK5S21 = TileCfg<5, 21, 7, 0>;    // 63 groups of 5 lanes, 11 warps
+using TileK3S11 = TileCfg<3, 11, 11, 0>;   // 11 groups of 3 lanes, 2 warps
+using TileK3S21 = TileCfg<3, 21, 7, 0>;    // 63 groups of 3 lanes, 7 warps
 
 template <class C>
 struct TileSmem {
@@ -1097,19 +1102,26 @@ namespace nlemk {
 
 bool nlem_tile_supported(const NlemLaunch& L) {
   // smaller (odd) windows run masked inside the kernel's grid
-  return (L.P.patch == 7 && L.P.search <= 21) || (L.P.patch == 5 && L.P.search <= 11);
+  return (L.P.patch == 7 || L.P.patch == 5 || L.P.patch == 3) && L.P.search <= 21;
 }
 
-
-cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream) {
-  if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream);
-  return launch_tile<TileK5S11>(L, stream);
+int nlem_tile_grid(const NlemLaunch& L) {  // side of the grid the serving instantiation uses
+  return L.P.patch == 7 || L.P.search > 11 ? 21 : 11;
 }
 
 cudaError_t launch_nlem_tile_list(const NlemLaunch& L, const int* list, const int* list_count,
                                   cudaStream_t stream) {
+  const bool big = nlem_tile_grid(L) == 21;
   if (L.P.patch == 7) return launch_tile<TileK7S21>(L, stream, list, list_count);
-  return launch_tile<TileK5S11>(L, stream, list, list_count);
+  if (L.P.patch == 5)
+    return big ? launch_tile<TileK5S21>(L, stream, list, list_count)
+               : launch_tile<TileK5S11>(L, stream, list, list_count);
+  return big ? launch_tile<TileK3S21>(L, stream, list, list_count)
+             : launch_tile<TileK3S11>(L, stream, list, list_count);
+}
+
+cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream) {
+  return launch_nlem_tile_list(L, nullptr, nullptr, stream);
 }
 
 }  // namespace nlemk

@@ -110,6 +110,7 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int
 bool irls_reg_supported(const IrlsLaunch& L);
 cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);
+int nlem_tile_grid(const NlemLaunch& L);  // grid side (21 or 11) of the tile instantiation for L
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);
 // tile kernel over a device-side list of band pixel indices (count read on the device)
 cudaError_t launch_nlem_tile_list(const NlemLaunch& L, const int* list, const int* list_count,

@@ -178,9 +178,12 @@ def test_small_window_shapes_vs_oracle(nb, oracle, monkeypatch, k, S, shape, for
         assert np.abs(fg - fo).max() <= TOL, (solver, k, S, shape, force)
 
 
-@pytest.mark.parametrize("k,S", [(7, 7), (7, 11), (7, 13), (7, 17), (5, 5)])
+@pytest.mark.parametrize("k,S", [(7, 7), (7, 11), (7, 13), (7, 17), (5, 5), (5, 13), (5, 21),
+                                 (3, 3), (3, 9), (3, 11), (3, 15), (3, 21)])
 def test_masked_window_all_solvers_and_bands(nb, oracle, k, S):
-    """Masked windows through every solver of the low-rank / tile kernels (ADMM at mu = 1, ADMM at
+    """Every odd patch side up to 7 with windows up to 21 is served by the low-rank kernel (k = 7) or
+    a tile-kernel instantiation (k = 7 / 5 / 3 on a 21 x 21 or 11 x 11 grid), smaller windows masked.
+    Masked windows through every solver of the low-rank / tile kernels (ADMM at mu = 1, ADMM at
     mu = 1e-3 with 8 sweeps - the hand-off to the exact tile kernel -, IRLS, NlmOnly; noisy and
     NLM init) vs the oracle, and a 3-band split with S/2 + k/2 halo rows (less than the kernels'
     fixed tile border: the band padding clamps) bitwise equal to the whole-image call."""
