@@ -1,0 +1,107 @@
+"""Turn the artefacts of tools/gpurun_r2_final.sh (gpurun_out/) into the committed round-2
+evidence under profiles/: ncu brief / opcode mix / executed FP32 flops / stall reasons / source
+hotspots of nlem_pixels_lr, the bench's launch list, the DRAM counters of the bench launch,
+profiles/ncu_summary.json (read by bench.py for roofline.executed / traffic) and the bench lines.
+
+    python tools/save_profiles_r2.py
+"""
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+os.chdir(ROOT)
+REP = "gpurun_out/r2_lr_full.ncu-rep"
+
+
+def run(cmd, out):
+    with open(out, "w") as f:
+        subprocess.run(cmd, stdout=f, stderr=subprocess.DEVNULL, check=False)
+
+
+run([sys.executable, "tools/dev/ncu_brief.py", REP], "profiles/r2_lr_brief.txt")
+run([sys.executable, "tools/dev/ncu_ops.py", REP], "profiles/r2_lr_opcodes.txt")
+run([sys.executable, "tools/ncu_lines.py", REP, "40"], "profiles/r2_lr_source_hotspots.txt")
+run([sys.executable, "tools/dev/ncu_stall_ops.py", REP], "profiles/r2_lr_stalls.txt")
+subprocess.run([sys.executable, "tools/ncu_flops.py", REP, "profiles/r2_lr_executed.json"],
+               stdout=subprocess.DEVNULL, check=True)
+
+# ---- launch list of the bench command
+rows = list(csv.reader(open("gpurun_out/r2_launches.csv")))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+h = rows[hi]
+agg = collections.OrderedDict()
+for r in rows[hi + 1:]:
+    d = dict(zip(h, r))
+    if d.get("Metric Name") != "gpu__time_duration.sum":
+        continue
+    v = float(d["Metric Value"].replace(",", ""))
+    u = d.get("Metric Unit", "ns")
+    ms = v * {"ns": 1e-6, "nsecond": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0,
+              "s": 1e3, "second": 1e3}[u]
+    a = agg.setdefault(d["Kernel Name"], [0, 0.0])
+    a[0] += 1
+    a[1] += ms
+tot = sum(v[1] for v in agg.values())
+out = ["ncu --metrics gpu__time_duration.sum --clock-control none  python bench.py --steps 2 --warmup 3 "
+       "--no-cpu-baseline --no-secondary",
+       "(cold-cache, serialised per-launch times; compare shares, not absolutes; final round-2 kernel)", ""]
+for k, (n, ms) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    out.append(f"{n:4d} launches {ms:13.3f} ms total {ms / tot * 100:8.3f}%  {k[:170]}")
+open("profiles/r2_launches_bench.txt", "w").write("\n".join(out) + "\n")
+
+# ---- DRAM counters of the bench's nlem_pixels_lr launches
+rows = list(csv.reader(open("gpurun_out/r2_dram.csv")))
+hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+h = rows[hi]
+L = collections.OrderedDict()
+for r in rows[hi + 1:]:
+    d = dict(zip(h, r))
+    L.setdefault(d["ID"], {"grid": d["Grid Size"]})[d["Metric Name"]] = (
+        float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
+tob = lambda v, u: v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
+tons = lambda v, u: v * {"ns": 1, "nsecond": 1, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6,
+                         "s": 1e9, "second": 1e9}[u]
+txt = ["ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \\",
+       "    -k regex:nlem_pixels_lr -c 4 python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-secondary",
+       "(one B200, final round-2 kernel; launches 0 / 2 = the small-mu probe, 64 CTAs; 1 / 3 = the main "
+       "4096x4096 launch, 148 CTAs)", "", "launch  grid  dram read (B)   dram write (B)   duration (ns)"]
+main = None
+for k, d in L.items():
+    rd, wr = tob(*d["dram__bytes_read.sum"]), tob(*d["dram__bytes_write.sum"])
+    ns = tons(*d["gpu__time_duration.sum"])
+    g = d["grid"].strip("()").split(",")[0]
+    txt.append(f"{k:<7s} {g:>4s} {rd:>14,.0f} {wr:>14,.0f} {ns:>15,.0f}")
+    if g == "148":
+        main = (rd, wr, ns)
+open("profiles/r2_lr_dram.txt", "w").write("\n".join(txt) + "\n")
+
+# ---- summary read by bench.py
+ex = json.load(open("profiles/r2_lr_executed.json"))
+s = json.load(open("profiles/ncu_summary.json"))
+px = 64 * 4096
+s.update({
+    "executed_fp32_flops_per_pixel": ex["executed_fp32_flops"] / px,
+    "fma_pipe_active_pct": ex["fma_pipe_active_pct"], "issue_active_pct": ex["issue_active_pct"],
+    "smem_wavefronts_pct": ex["smem_wavefronts_pct"],
+    "smem_wavefronts_per_pixel": ex["smem_wavefronts"] / px,
+    "dram_bytes_per_launch": int(main[0] + main[1]),
+    "executed_source": "profiles/r2_lr_executed.json (ncu --set full --clock-control none, one launch on a "
+                       "64-row config-3 band = 262,144 pixels, final round-2 kernel, tools/gpurun_r2_final.sh)",
+    "dram_source": "profiles/r2_lr_dram.txt: ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,"
+                   "gpu__time_duration.sum --clock-control none -k regex:nlem_pixels_lr -c 4 python bench.py "
+                   "--steps 1 --warmup 1 --no-cpu-baseline --no-secondary (main 4096^2 launch: "
+                   f"{main[0] / 1e6:.1f} MB read + {main[1] / 1e6:.1f} MB written vs 136 MB algorithmic: the "
+                   "padded band once, the output once - no re-reads)"})
+json.dump(s, open("profiles/ncu_summary.json", "w"), indent=1)
+for src, dst in (("gpurun_out/bench_full.log", "profiles/r2_bench_line.json"),
+                 ("gpurun_out/bench_ref.log", "profiles/r2_bench_reference_line.json")):
+    line = open(src).read().strip().splitlines()[-1]
+    json.loads(line)
+    open(dst, "w").write(line + "\n")
+d = json.load(open("profiles/r2_bench_line.json"))
+print("value", d["value"], "e2e", d["e2e"]["value"], "frac", d["roofline"]["frac"], "executed",
+      d["roofline"]["executed"]["frac_executed"], "parity", d["parity"]["max_abs_diff"])
