@@ -76,6 +76,10 @@ struct TileCfg {
   static constexpr int CSTR = (KS + 3) / 4 * 4 + ((((KS + 3) / 4) % 2) ? 0 : 4);
   static constexpr int CSN = (KS * CSTR + 3) & ~3;
   static constexpr int THREADS = 32 * WARPS;
+  // resident CTAs per SM the register budget is capped for: the 2-warp instantiations (11 x 11
+  // grids) need many pixels in flight per SM (8 CTAs = 128 registers: k=5/S=11 74 vs 55 Mpix/s
+  // at 5 CTAs of 180 registers; 10 and more spill and lose), the 21 x 21 ones are one CTA per SM
+  static constexpr int MINB = THREADS <= 64 ? 8 : 1;
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
   static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
@@ -387,7 +391,7 @@ __device__ __forceinline__ float block_sum_scalar(TileCtx<C>& X, float v) {
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS, 1)
+__global__ void __launch_bounds__(C::THREADS, C::MINB)
 nlem_pixels_tile(const float* __restrict__ pad, int64_t pad_cols, int64_t rows, int64_t cols,
                  int64_t out_row0, int64_t out_rows, NlemDevParams P, float* out, float* frames,
                  int* work_counter, int chunk, FailureSlot* fail, const int* list,
