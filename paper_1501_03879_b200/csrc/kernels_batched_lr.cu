@@ -61,7 +61,6 @@ constexpr int KR = 4, KS = 4, KP = KR + KS;  // float2 point pairs per group: re
 constexpr int WARPS = 7;                     // point warps
 constexpr int CW = WARPS;                    // the consensus warp (no points)
 constexpr int NW = WARPS + 1, ALL = 32 * NW;
-constexpr int PT = 32 * WARPS;               // point threads
 constexpr int GPW = 32 / G, NG = GPW * WARPS, NCAP = NG * 2 * KP;  // 28 groups, 448 points
 constexpr int R = 4;
 constexpr int TM_HALF = KS * J * 2;          // TMEM columns per lane: the second half of its points
