@@ -257,16 +257,16 @@ __device__ __forceinline__ void fold_store(float (&v)[J], float v7, float* row, 
     float4* d = reinterpret_cast<float4*>(row + 8 * (lane & (G - 1)));
     d[0] = make_float4(v[0], v[1], v[2], v[3]);
     d[1] = make_float4(v[4], v[5], v[6], v7);
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int o = G; o < 32; o <<= 1)
+    for (int o = G; o < 32; o <<= 1)
 #pragma unroll
-    for (int i = 0; i < J; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-  if (lane < G) {
-    float4* d = reinterpret_cast<float4*>(row + 8 * lane);
-    d[0] = make_float4(v[0], v[1], v[2], v[3]);
-    d[1] = make_float4(v[4], v[5], v[6], v7);
+      for (int i = 0; i < J; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    if (lane < G) {
+      float4* d = reinterpret_cast<float4*>(row + 8 * lane);
+      d[0] = make_float4(v[0], v[1], v[2], v[3]);
+      d[1] = make_float4(v[4], v[5], v[6], v7);
+    }
   }
 }
 // Column pair (2 lane, 2 lane + 1) summed over the NR partial rows in a fixed tree.
