@@ -1,5 +1,6 @@
-// Low-rank ("Gram-form") NLEM / EM-ADMM kernel for k = 7, S = 21 (configs 2, 3, 4); also the
-// IRLS comparator and the NlmOnly solver / nlm_denoise baseline in the same mapping.
+// Low-rank ("Gram-form") NLEM / EM-ADMM kernel for k = 7, S <= 21 (configs 2, 3, 4; windows
+// smaller than 21 run masked inside the 21 x 21 grid); also the IRLS comparator and the NlmOnly
+// solver / nlm_denoise baseline in the same mapping.
 //
 // Algebra (p-form of admm.hpp:49-78).  With p_k = z - y_k/mu - a_k and
 // s_k = min(1, lambda_k / ||p_k||), one sweep is
