@@ -79,7 +79,8 @@ struct TileCfg {
   // resident CTAs per SM the register budget is capped for: the 2-warp instantiations (11 x 11
   // grids) need many pixels in flight per SM (8 CTAs = 128 registers: k=5/S=11 74 vs 55 Mpix/s
   // at 5 CTAs of 180 registers; 10 and more spill and lose), the 21 x 21 ones are one CTA per SM
-  static constexpr int MINB = THREADS <= 64 ? 8 : 1;
+  // (k=5 / k=3 on the 21 x 21 grid: 2 / 3 CTAs measured best: 13.9 vs 12.2 and 28.0 vs 25.2 Mpix/s)
+  static constexpr int MINB = THREADS <= 64 ? 8 : (THREADS >= 512 ? 1 : (KS == 5 ? 2 : 3));
   static constexpr int KP = KB / 2;              // point pairs per lane
   static constexpr bool ODD = (KB % 2) != 0;     // one unpaired point
   static constexpr int SEG = KB + KS - 1;        // tile values a lane touches
