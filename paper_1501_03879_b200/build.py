@@ -17,7 +17,8 @@ SO = os.path.join(OUT_DIR, "libnlem_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 CU_SOURCES = ["abi.cu", "kernels_generic.cu", "kernels_fast.cu", "kernels_nlem_tile.cu",
-              "kernels_nlem_lr.cu", "kernels_batched_lr.cu", "kernels_aux.cu"]
+              "kernels_nlem_lr.cu", "kernels_nlem_lr_r12.cu", "kernels_batched_lr.cu",
+              "kernels_aux.cu"]
 CXX_SOURCES = ["synth.cpp", "multi_host.cpp"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -589,14 +589,19 @@ nlem_status denoise_rows_impl(const float* noisy, int64_t in_row0, int64_t in_ro
                  dp, out, frames, reinterpret_cast<FailureSlot*>(slot.ptr)};
     if (kind == Kind::LR) {
       // low-rank kernel, then the exact tile kernel over the pixels it handed off
-      // [0] work counter, [1] hand-off count (-1: all), [2, 3] small-mu probe, [4..] hand-off list
+      // [0] work counter, [1] hand-off count (-1: all), [2, 3] small-mu probe, [4] work counter
+      // of the ring-12 launch, [8..] hand-off list
       int* scratch = nullptr;
       const int64_t pixels = out_rows * cols;
-      e = cudaMallocAsync(&scratch, (4 + pixels) * sizeof(int), s);
-      if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 4 * sizeof(int), s);
+      e = cudaMallocAsync(&scratch, (8 + pixels) * sizeof(int), s);
+      if (e == cudaSuccess) e = cudaMemsetAsync(scratch, 0, 8 * sizeof(int), s);
       int* probe = nlem_lr_probe_wanted(L) ? scratch + 2 : nullptr;
-      if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 4, scratch + 1, scratch, probe, s);
-      if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 4, scratch + 1, s);
+      if (e == cudaSuccess) e = launch_nlem_lr(L, scratch + 8, scratch + 1, scratch, probe, s);
+      // small-mu regime with up to kLrBigRing sweeps: the ring-12 build takes the band (it
+      // returns at once when the probe did not find that regime)
+      if (e == cudaSuccess && probe != nullptr && L.P.iters <= kLrBigRing)
+        e = launch_nlem_lr_ring12(L, scratch + 8, scratch + 1, scratch + 4, probe, s);
+      if (e == cudaSuccess) e = launch_nlem_tile_list(L, scratch + 8, scratch + 1, s);
       const bool stats = std::getenv("NLEM_LR_STATS") != nullptr;  // read per call (tests)
       if (stats && e == cudaSuccess) {  // diagnostics only: synchronises the stream
         int handed = 0;

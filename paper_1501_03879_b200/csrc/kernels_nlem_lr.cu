@@ -75,8 +75,22 @@ static_assert((PB - PA) % 32 == 12 && PB >= TH * PCS, "copy B placement");
 #endif
 constexpr int WARPS = NLEM_LR_WARPS;  // pixel-warps per CTA (1 CTA per SM)
 constexpr int SEGL = 7;  // points per segment
-constexpr int R = 4;     // history ring
-constexpr int NF = 8;    // state fields per point in TMEM
+// History ring length.  4 in the production build (16 pixel-warps per SM); the second
+// translation unit kernels_nlem_lr_r12.cu compiles this file with NLEM_LR_R = 12 and 8 warps
+// for the small-mu regime (prox scales of 1: no history term decays, so the ring must hold all
+// T <= 12 sweeps; twice the tensor-memory columns per pixel, hence half the warps).
+#ifndef NLEM_LR_R
+#define NLEM_LR_R 4
+#endif
+constexpr int R = NLEM_LR_R;
+constexpr int NF = 4 + R;       // state fields per point in TMEM: H, K, ga, ||a~||^2, al_0..R-1
+constexpr int PC = 2 * NF;      // TMEM columns of one point pair (16 or 32)
+constexpr int TCW = R == 4 ? 128 : 256;  // TMEM columns per pixel-warp
+static_assert(PC == 16 || PC == 32, "point pairs move as one or two x16 accesses");
+static_assert(SEGL * PC + 16 <= TCW && (WARPS / 4) * TCW <= 512 && WARPS % 4 == 0, "TMEM budget");
+#ifndef NLEM_LR_NAME
+#define NLEM_LR_NAME nlem_pixels_lr
+#endif
 // unroll factors of the correlation loops over patch columns (A/B build variants)
 #ifndef NLEM_LR_UD
 #define NLEM_LR_UD 7  // A/B on the paired layout: 7 (unrolled) 32.23 vs 1 (rolled) 32.00 Mpix/s
@@ -86,9 +100,6 @@ constexpr int NF = 8;    // state fields per point in TMEM
 #endif
 #define LR_PRAGMA(x) _Pragma(#x)
 #define LR_UNROLL(n) LR_PRAGMA(unroll n)
-#ifndef NLEM_LR_ST
-#define NLEM_LR_ST 2  // columns per tcgen05.st in the sweep (1, 2 or 4)
-#endif
 constexpr int RED_STR = 36;
 constexpr int CB_STR = 8;
 // per-warp shared memory (floats)
@@ -96,7 +107,7 @@ constexpr int W_RED = TILE;  // single tile buffer
 constexpr int W_CB = W_RED + 32 * RED_STR;
 constexpr int W_OWN = W_CB + KS * CB_STR;        // [4 + 2 (R+1)][32] owner scalars
 constexpr int W_NR = W_OWN + (4 + 2 * (R + 1)) * 32;  // [R+1] (+pad) ||c~||^2 ring
-constexpr int W_TOTAL = W_NR + 8;
+constexpr int W_TOTAL = W_NR + ((R + 1 + 3) & ~3);
 constexpr size_t SMEM_BYTES = size_t(WARPS) * W_TOTAL * sizeof(float) + 16;
 constexpr int kProbe = 1024;  // pixels sampled by the small-mu probe launch
 constexpr int kCenterLane = 24;  // owner of coordinate D/2 = (3, 3): half A row 3*7+3
@@ -311,21 +322,27 @@ __device__ __forceinline__ float row_sum(const float* row) {
 using namespace lr;
 
 __global__ void __launch_bounds__(WARPS * 32, 1)
-nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, int out_row0,
+NLEM_LR_NAME(const float* __restrict__ pad, int pad_cols, int rows, int cols, int out_row0,
                int plane, NlemDevParams P, float* out, float* frames, int* work_counter,
                int* ovf_list, int* ovf_count, FailureSlot* fail, int probe_n, int* probe_count) {
   // probe_n > 0 (probe launch): only the setup and the small-mu predictor of probe_n pixels
   // spread evenly over the band, counting predicted hand-offs into *probe_count; no outputs.
   // probe_n == 0 with probe_count (main launch): when more than 90 % of the probe pixels
-  // would be handed off (the small-mu regime), every pixel is: *ovf_count = -1 tells the tile
-  // kernel to take the whole band, and this launch does no pixel work.  The decision depends on
-  // the input only (deterministic).
+  // would be handed off (the small-mu regime), this launch does no pixel work: up to
+  // kLrBigRing sweeps the ring-12 build of this kernel (launched next) takes the band, beyond
+  // that *ovf_count = -1 tells the tile kernel to.  The ring-12 launch in turn only works in
+  // that regime.  The decision depends on the input only (deterministic).
   if (probe_n == 0 && probe_count != nullptr) {
     const int pt = plane < kProbe ? plane : kProbe;
-    if (10 * *static_cast<volatile int*>(probe_count) > 9 * pt) {
-      if (blockIdx.x == 0 && threadIdx.x == 0) *ovf_count = -1;
+    const bool small_mu = 10 * *static_cast<volatile int*>(probe_count) > 9 * pt;
+#ifdef NLEM_LR_SECONDARY
+    if (!small_mu) return;
+#else
+    if (small_mu) {
+      if (P.iters > kLrBigRing && blockIdx.x == 0 && threadIdx.x == 0) *ovf_count = -1;
       return;
     }
+#endif
   }
   extern __shared__ __align__(16) float smem[];
   // warp index through a shuffle: the compiler then knows it is warp-uniform (uniform datapath)
@@ -349,15 +366,15 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tbase = *tm_base_slot;
   const uint32_t tw = tbase + (static_cast<uint32_t>((warp & 3) * 32) << 16) +
-                      static_cast<uint32_t>((warp >> 2) * 128);
+                      static_cast<uint32_t>((warp >> 2) * TCW);
   // TMEM addresses are formed right before each access (opaque to CSE/hoisting): kept as
   // long-lived uniform registers they exhaust the uniform register file and spill
   auto t_at = [&](uint32_t col) { return tw + col; };
   // column layout per lane: point pair i (slot 0 and slot 1 point i) = 16 columns, field q of
   // slot s at 2 q + s, so one x16 load yields 8 (slot 0, slot 1) register pairs for the paired
   // (FFMA2 / FMUL2 / FADD2) scalar update; lambdas of the 14 points at 112 + 2 i + s
-  auto t_pt = [&](int i) { return t_at(static_cast<uint32_t>(i * 2 * NF)); };
-  auto t_lam = [&]() { return t_at(static_cast<uint32_t>(2 * NF * SEGL)); };
+  auto t_pt = [&](int i) { return t_at(static_cast<uint32_t>(i * PC)); };
+  auto t_lam = [&]() { return t_at(static_cast<uint32_t>(PC * SEGL)); };
 
   // lane geometry: segment column offsets in the tile
   int sgx0, sgy00, sgx1, sgy01;
@@ -523,6 +540,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         const float st[16] = {A2[i].x, A2[i].y, -A2[i].x, -A2[i].y, 0.0f, 0.0f, A2[i].x, A2[i].y,
                               0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
         tm_st<16>(t_pt(i), st);
+        if constexpr (PC == 32) {  // al_4 .. al_{R-1} = 0
+          const float z16[16] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f,
+                                 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+          tm_st<16>(t_pt(i) + 16, z16);
+        }
       }
       tm_st<16>(t_lam(), lm);
       }
@@ -533,8 +555,13 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 
     // ---- patch-sum pass (sum_k u_k a_k per coordinate) + transpose reduction to the owners.
     // Half A rows (jx - 0) * 7 + jy, half B rows (jx - 4) * 7 + jy, then 5 extra scalars.
-    auto patch_sum_reduce = [&](const float2 (&u2)[SEGL], const float (&extra)[5], float& oA,
-                                float& oB, float (&xs)[5]) {
+    // NEX extra per-lane scalars ride along as rows of their own: all after half B's 21
+    // coordinate rows when they fit the 32-row buffer (NEX <= 11), otherwise the first four after
+    // half A's 28 rows and the rest after half B's.
+    auto patch_sum_reduce = [&]<int NEX>(const float2 (&u2)[SEGL], const float (&extra)[NEX],
+                                         float& oA, float& oB, float (&xs)[NEX]) {
+      constexpr int EXA = NEX <= 11 ? 0 : 4;  // extras summed with half A
+      static_assert(3 * KS + NEX - EXA <= 32, "transpose buffer rows");
       LR_FSTART()
 #pragma unroll
       for (int hf = 0; hf < 2; ++hf) {
@@ -553,7 +580,10 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         }
         if (hf) {
 #pragma unroll
-          for (int q = 0; q < 5; ++q) red[(3 * KS + q) * RED_STR + lane] = extra[q];
+          for (int q = EXA; q < NEX; ++q) red[(3 * KS + q - EXA) * RED_STR + lane] = extra[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < EXA; ++q) red[(4 * KS + q) * RED_STR + lane] = extra[q];
         }
         LR_FSTAMP(hf ? 3 : 0)
         __syncwarp();
@@ -565,10 +595,12 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         LR_FSTAMP(hf ? 5 : 2)
         if (hf == 0) {
           oA = rr;
+#pragma unroll
+          for (int q = 0; q < EXA; ++q) xs[q] = __shfl_sync(0xffffffffu, rr, 4 * KS + q);
         } else {
           oB = rr;
 #pragma unroll
-          for (int q = 0; q < 5; ++q) xs[q] = __shfl_sync(0xffffffffu, rr, 3 * KS + q);
+          for (int q = EXA; q < NEX; ++q) xs[q] = __shfl_sync(0xffffffffu, rr, 3 * KS + q - EXA);
         }
       }
     };
@@ -629,7 +661,10 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
     { const long long q_ = clock64(); st_p[3] += q_ - st_q; st_q = q_; }
 #endif
     // ring slots: sl[q] holds c~_{t-q} (q < R), sl[R] is the free slot; rotated once per sweep
-    int sl[R + 1] = {0, 4, 3, 2, 1};
+    int sl[R + 1];
+    sl[0] = 0;
+#pragma unroll
+    for (int q = 1; q <= R; ++q) sl[q] = R + 1 - q;
     // Publish c~_{t+1} and form the Gram row <c~_{t-q}, c~_{t+1}> of the coming sweep.  The row
     // stays in registers (every lane holds the butterfly result) and the owners pass c~_{t+1}, m
     // and the four history vectors they already loaded for the consensus, so only c~ itself goes
@@ -692,7 +727,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         float2 beta[SEGL];
         float bsum = 0.0f, ssum = 0.0f;
         float wl[16];
-        tm_ld16c_wait<2 * NF * SEGL>(tw, wl);
+        tm_ld16c_wait<PC * SEGL>(tw, wl);
 #pragma unroll
         for (int i = 0; i < SEGL; ++i) {
           // one hardware reciprocal square root per point (rsqrt.approx, ~2 ulp)
@@ -738,9 +773,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       if (ifail_iter < 0) iters = stop_at > 0 ? stop_at : P.iters;
     } else {
     {
-      const float zero4[R] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float zeroR[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) zeroR[q] = 0.0f;
       __syncwarp();  // the owners' initial rows (and the cleared norm ring) are visible
-      publish_regs(own[4 * 32], own[(4 + R + 1) * 32], own[2 * 32], own[3 * 32], zero4, zero4);
+      publish_regs(own[4 * 32], own[(4 + R + 1) * 32], own[2 * 32], own[3 * 32], zeroR, zeroR);
     }
 #ifdef NLEM_LR_STAMPS
     st_t2 = clock64(); st_setup += st_t2 - st_t1;
@@ -755,7 +792,9 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       // per slot: (1) dot products D_k = <a_k - m, c~>, (2) scalar update of the 7 points
       // (state in TMEM)
       float2 u[SEGL];  // ga' of (slot 0, slot 1): the FFMA2 pairs of the patch-sum pass
-      float vac[R] = {0.0f, 0.0f, 0.0f, 0.0f};
+      float vac[R];
+#pragma unroll
+      for (int q = 0; q < R; ++q) vac[q] = 0.0f;
       float usum = 0.0f;
       bool fnorm = false, sne1 = false;
       float2 Dk2[SEGL];
@@ -784,7 +823,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
 #endif
       {
         float lm[16];
-        tm_ld16c_wait<2 * NF * SEGL>(tw, lm);
+        tm_ld16c_wait<PC * SEGL>(tw, lm);
         float G[R];
 #pragma unroll
         for (int q = 0; q < R; ++q) G[q] = gq[q];
@@ -801,25 +840,35 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
         float2 nchk = make_float2(0.0f, 0.0f);
         float hmax = -1.0f;
         // the state of point pair i + 1 is requested before the arithmetic of pair i
-        uint32_t stq[2][16];
+        uint32_t stq[2][PC];
+        auto issue_pair = [&](auto ic, uint32_t (&dst)[PC]) {
+          constexpr int i = decltype(ic)::value;
+          tm::ld16_issue<i * PC>(tw, reinterpret_cast<uint32_t(&)[16]>(dst[0]));
+          if constexpr (PC == 32) tm::ld16_issue<i * PC + 16>(tw, reinterpret_cast<uint32_t(&)[16]>(dst[16]));
+        };
+        auto wait_pair = [&](uint32_t (&dst)[PC]) {
+          tm::wait_ld(reinterpret_cast<uint32_t(&)[16]>(dst[0]));
+          if constexpr (PC == 32) tm::wait_ld(reinterpret_cast<uint32_t(&)[16]>(dst[16]));
+        };
         tm_wait_st();  // the previous sweep's state stores (they had three phases to land)
-        tm::ld16_issue<0>(tw, stq[0]);
+        issue_pair(std::integral_constant<int, 0>{}, stq[0]);
         static_for<SEGL>([&](auto ic) {
           constexpr int i = decltype(ic)::value;
           // point i of both slots as one register pair per field
-          float st[16];
-          tm::wait_ld(stq[i & 1]);
+          float st[PC];
+          wait_pair(stq[i & 1]);
 #pragma unroll
-          for (int q = 0; q < 16; ++q) st[q] = __uint_as_float(stq[i & 1][q]);
-          if constexpr (i + 1 < SEGL) tm::ld16_issue<(i + 1) * 2 * NF>(tw, stq[(i + 1) & 1]);
+          for (int q = 0; q < PC; ++q) st[q] = __uint_as_float(stq[i & 1][q]);
+          if constexpr (i + 1 < SEGL) issue_pair(std::integral_constant<int, i + 1>{}, stq[(i + 1) & 1]);
           const float2 H = make_float2(st[0], st[1]), K = make_float2(st[2], st[3]);
           const float2 ga = make_float2(st[4], st[5]), a2 = make_float2(st[6], st[7]);
-          const float2 al0 = make_float2(st[8], st[9]), al1 = make_float2(st[10], st[11]);
-          const float2 al2 = make_float2(st[12], st[13]), al3 = make_float2(st[14], st[15]);
+          float2 al[R];
+#pragma unroll
+          for (int q = 0; q < R; ++q) al[q] = make_float2(st[8 + 2 * q], st[9 + 2 * q]);
           const float2 D_ = __fadd2_rn(Dk2[i], make_float2(-Cm, -Cm));
-          const float2 X2 = __ffma2_rn(al0, make_float2(G[0], G[0]),
-                            __ffma2_rn(al1, make_float2(G[1], G[1]),
-                            __ffma2_rn(al2, make_float2(G[2], G[2]), __fmul2_rn(al3, make_float2(G[3], G[3])))));
+          float2 X2 = __fmul2_rn(al[R - 1], make_float2(G[R - 1], G[R - 1]));
+#pragma unroll
+          for (int q = R - 2; q >= 0; --q) X2 = __ffma2_rn(al[q], make_float2(G[q], G[q]), X2);
           const float2 gp1 = __fadd2_rn(ga, one2);
           const float2 t2 = __ffma2_rn(make_float2(-gp1.x, -gp1.y), D_, X2);
           const float2 HG = __fadd2_rn(H, make_float2(Gnn, Gnn));
@@ -833,11 +882,11 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
             sc.y = ly != 0.0f ? fminf(1.0f, ly * rsq(Nc.y)) : 0.0f;
           }
           const float2 B = __fadd2_rn(K, D_);
-          const float2 ev = __fmul2_rn(sc, al3);
+          const float2 ev = __fmul2_rn(sc, al[R - 1]);
           const float2 evv = __fmul2_rn(__fmul2_rn(ev, ev), make_float2(nrR, nrR));
           // hand-off tests as one running maximum (positive = hand the pixel to the exact
           // kernel), checked once per sweep:
-          //  * ring overflow: the dropped term s al_3 c~_{t-R} is above FP32 rounding of p;
+          //  * ring overflow: the dropped term s al_{R-1} c~_{t-R} is above FP32 rounding of p;
           //  * cancellation of the Gram expansion: ||p||^2 far below the terms it is formed from
           //    (N < 2^-8 (H + ||c~||^2)), so FP32 rounding of N would be amplified into s (the
           //    batched kernel's test, kernels_batched_lr.cu).  Padding points (lambda = 0) are
@@ -846,37 +895,28 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           const float2 vc = __ffma2_rn(HG, make_float2(kCancel, kCancel), make_float2(-N.x, -N.y));
           hmax = max3(hmax, vo.x, vo.y);
           hmax = max3(hmax, vc.x, vc.y);
-          float o[16];
+          float o[PC];
           const float2 oH = __ffma2_rn(sc, __ffma2_rn(sc, Nc, __fmul2_rn(make_float2(-2.0f, -2.0f), B)), a2);
           const float2 oK = __ffma2_rn(sc, B, make_float2(-a2.x, -a2.y));
           const float2 oga = __fmul2_rn(sc, gp1);
-          const float2 o1 = __fmul2_rn(sc, al0), o2 = __fmul2_rn(sc, al1), o3 = __fmul2_rn(sc, al2);
           o[0] = oH.x; o[1] = oH.y; o[2] = oK.x; o[3] = oK.y; o[4] = oga.x; o[5] = oga.y;
-          o[6] = a2.x; o[7] = a2.y; o[8] = sc.x; o[9] = sc.y; o[10] = o1.x; o[11] = o1.y;
-          o[12] = o2.x; o[13] = o2.y; o[14] = o3.x; o[15] = o3.y;
+          o[6] = a2.x; o[7] = a2.y; o[8] = sc.x; o[9] = sc.y;
           vac2[0] = __fadd2_rn(vac2[0], sc);
-          vac2[1] = __fadd2_rn(vac2[1], o1);
-          vac2[2] = __fadd2_rn(vac2[2], o2);
-          vac2[3] = __fadd2_rn(vac2[3], o3);
+#pragma unroll
+          for (int q = 1; q < R; ++q) {  // al'_q = s al_{q-1}
+            const float2 oq = __fmul2_rn(sc, al[q - 1]);
+            o[8 + 2 * q] = oq.x;
+            o[9 + 2 * q] = oq.y;
+            vac2[q] = __fadd2_rn(vac2[q], oq);
+          }
           u[i] = oga;
           us2 = __fadd2_rn(us2, oga);
-#if NLEM_LR_ST == 4
-          static_for<4>([&](auto qc) {
-            constexpr int q = decltype(qc)::value;
-            tm_st4c<i * 2 * NF + 4 * q>(tw, o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-          });
-#elif NLEM_LR_ST == 2
-          static_for<8>([&](auto qc) {
+          // two columns per store (wider register tuples fragment the register file: spills)
+          static_for<NF>([&](auto qc) {
             constexpr int q = decltype(qc)::value;
             if constexpr (q != 3)  // field 3 (||a~||^2) never changes: not rewritten
-              tm_st2c<i * 2 * NF + 2 * q>(tw, o[2 * q], o[2 * q + 1]);
+              tm_st2c<i * PC + 2 * q>(tw, o[2 * q], o[2 * q + 1]);
           });
-#else
-          static_for<16>([&](auto qc) {
-            constexpr int q = decltype(qc)::value;
-            tm_st1c<i * 2 * NF + q>(tw, o[q]);
-          });
-#endif
         });
 #pragma unroll
         for (int q = 0; q < R; ++q) vac[q] = vac2[q].x + vac2[q].y;
@@ -890,7 +930,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
           static_for<SEGL>([&](auto ic) {
             constexpr int i = decltype(ic)::value;
             float st[16];
-            tm_ld16c_wait<i * 2 * NF>(tw, st);
+            tm_ld16c_wait<i * PC>(tw, st);
             sne1 |= (((realmask >> i) & 1u) && st[8] != 1.0f) ||
                     (((realmask >> (SEGL + i)) & 1u) && st[9] != 1.0f);
           });
@@ -898,12 +938,15 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
       }
       // a ring overflow / cancellation hands the whole pixel to the exact kernel: stop now
       // (3) g = sum_k ga'_k a_k per coordinate, reduced with usum and the history sums
-      float gA, gB, xs[5];
+      float gA, gB, xs[1 + R];
 #ifdef NLEM_LR_STAMPS
       { const long long q_ = clock64(); st_s[1] += q_ - st_sq; st_sq = q_; }
 #endif
       {
-        const float ex[5] = {usum, vac[0], vac[1], vac[2], vac[3]};
+        float ex[1 + R];
+        ex[0] = usum;
+#pragma unroll
+        for (int q = 0; q < R; ++q) ex[1 + q] = vac[q];
         patch_sum_reduce(u, ex, gA, gB, xs);
       }
 #ifdef NLEM_LR_STAMPS
@@ -1029,6 +1072,7 @@ nlem_pixels_lr(const float* __restrict__ pad, int pad_cols, int rows, int cols, 
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
+#ifndef NLEM_LR_SECONDARY
 bool nlem_lr_supported(const NlemLaunch& L) {
   // 32-bit pixel indexing inside the kernel
   const int64_t lim = int64_t(1) << 30;
@@ -1044,7 +1088,7 @@ bool nlem_lr_probe_wanted(const NlemLaunch& L) {
 
 cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
                            int* probe, cudaStream_t stream) {
-  auto kfn = nlem_pixels_lr;
+  auto kfn = NLEM_LR_NAME;
   cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(SMEM_BYTES));
   if (e != cudaSuccess) return e;
@@ -1066,5 +1110,25 @@ cudaError_t launch_nlem_lr(const NlemLaunch& L, int* ovf_list, int* ovf_count, i
       ovf_list, ovf_count, L.fail, 0, probe);
   return cudaGetLastError();
 }
+
+#else
+// The ring-12 build (kernels_nlem_lr_r12.cu): launched after launch_nlem_lr when a probe ran and
+// 4 < T <= kLrBigRing; it returns at once unless the probe found the small-mu regime.
+cudaError_t launch_nlem_lr_ring12(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
+                                  int* probe, cudaStream_t stream) {
+  static_assert(R == kLrBigRing, "ring length of the secondary build");
+  auto kfn = NLEM_LR_NAME;
+  cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(SMEM_BYTES));
+  if (e != cudaSuccess) return e;
+  const int64_t pixels = L.out_rows * L.cols;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(device_caps().sms, (pixels + WARPS - 1) / WARPS));
+  kfn<<<static_cast<unsigned>(grid), WARPS * 32, SMEM_BYTES, stream>>>(
+      L.pad, static_cast<int>(L.pad_cols), static_cast<int>(L.rows), static_cast<int>(L.cols),
+      static_cast<int>(L.out_row0), static_cast<int>(pixels), L.P, L.out, L.frames, counter,
+      ovf_list, ovf_count, L.fail, 0, probe);
+  return cudaGetLastError();
+}
+#endif
 
 }  // namespace nlemk

@@ -109,6 +109,11 @@ cudaError_t launch_admm_lr(const AdmmLaunch& L, int* ho_list, int* ho_count, int
 // Register-resident batched IRLS for d = 49 (kernels_batched_lr.cu).
 bool irls_reg_supported(const IrlsLaunch& L);
 cudaError_t launch_irls_reg(const IrlsLaunch& L, cudaStream_t stream);
+// ring length of the low-rank kernel's second build (kernels_nlem_lr_r12.cu): the most sweeps it
+// runs in the small-mu regime
+constexpr int kLrBigRing = 12;
+cudaError_t launch_nlem_lr_ring12(const NlemLaunch& L, int* ovf_list, int* ovf_count, int* counter,
+                                  int* probe, cudaStream_t stream);
 bool nlem_tile_supported(const NlemLaunch& L);
 int nlem_tile_grid(const NlemLaunch& L);  // grid side (21 or 11) of the tile instantiation for L
 cudaError_t launch_nlem_tile(const NlemLaunch& L, cudaStream_t stream);

@@ -395,26 +395,30 @@ def _run_forced_kernel(kernel, img, kw, tmp_path, stats=None):
 
 def test_lr_ring_handoff_small_mu(nb, oracle, tmp_path):
     """mu = 1e-3 (the reference default, types.hpp:121): lambda = w/mu ~ 1000 makes s_k = 1 for
-    most points, so the low-rank kernel's history ring cannot drop terms and hands the pixels to
-    the exact p-form tile kernel through its device-side list.  Frames and output vs oracle."""
+    most points, so no history term decays and the R = 4 ring of the production build cannot hold
+    the sweeps.  Up to 12 sweeps the ring-12 build of the low-rank kernel takes the band (no
+    hand-off); beyond that the pixels go to the exact p-form tile kernel through the device-side
+    list.  Frames and output vs the oracle in both regimes, both inits."""
     from paper_1501_03879_b200 import synth
 
     clean, noisy = synth.noisy_image(36, 36, 5, 3, 20.0)
-    for init in ("nlm", "noisy"):
-        g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(20.0, 49), iters=8,
-                            mu=1e-3, init=init)
-        fg = nb.nlem_denoise_snapshots(noisy, g)
-        _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
-        assert np.abs(fg - fo).max() <= TOL
-    # the hand-off path really ran (and the config-like mu = 1 case hands nothing off)
-    for mu, expect_handoff in ((1e-3, True), (1.0, False)):
+    for iters in (8, 12, 16):
+        for init in ("nlm", "noisy"):
+            g, o = _params_pair(nb, oracle, search=21, patch=7, h=synth.reference_h(20.0, 49),
+                                iters=iters, mu=1e-3, init=init)
+            fg = nb.nlem_denoise_snapshots(noisy, g)
+            _, fo = oracle.nlem_denoise(noisy.astype(np.float64), o, snapshots=True)
+            assert np.abs(fg - fo).max() <= TOL, (iters, init)
+    # which path really ran: ring-12 (nothing handed off) up to 12 sweeps, the tile kernel beyond;
+    # the config-like mu = 1 case hands nothing off either
+    for mu, iters, expect_handoff in ((1e-3, 8, False), (1e-3, 16, True), (1.0, 8, False)):
         stats = []
         kw = dict(search=21, patch=7, h=synth.reference_h(20.0, 49), solver="admm",
-                  solver_iters=8, mu=mu, init_mode="nlm")
+                  solver_iters=iters, mu=mu, init_mode="nlm")
         _run_forced_kernel("lr", noisy, kw, tmp_path, stats)
         handed = [int(l.split(",")[1].split()[0]) for l in stats]
         assert handed, stats
-        assert (sum(handed) > 0) == expect_handoff, stats
+        assert (sum(handed) > 0) == expect_handoff, (mu, iters, stats)
 
 
 def test_reference_default_params_in_lr_kernel(nb, oracle, tmp_path):
