@@ -425,7 +425,8 @@ def main():
         secondary["note"] = ("device-resident, CUDA events, L2 flushed; config 1 = BASELINE "
                              "configs[1] (65,536 x n=441 x d=49, T=50, mu=1), config 2 = 512^2; "
                              "*_small_mu = the reference's default mu = 1e-3 at T = 10 "
-                             "(exact p-form kernels after the small-mu probe)")
+                             "(after the small-mu probe: config-3 band in the ring-12 build of "
+                             "the low-rank kernel, config 1 in the exact p-form kernel)")
 
     value = rows * cols / (total_ms / args.steps / 1e3) / 1e6
     summary = load_profile_summary()

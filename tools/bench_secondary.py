@@ -102,7 +102,8 @@ def measure(problems=65536, reps=3):
     res["config1_small_mu"] = {"mu": 1e-3, "iters": 10, "problems_per_s": B / (ms / 1e3), "ms": ms,
                                "path": "small_mu_probe_kernel -> exact p-form kernel (admm_batched_fast)"}
     del P, W
-    # config-3 band (512 rows x 4096) at mu = 1e-3, T = 10: probe -> exact tile kernel for the band
+    # config-3 band (512 rows x 4096) at mu = 1e-3, T = 10: probe -> ring-12 build of the low-rank
+    # kernel (T <= 12; the exact tile kernel beyond)
     _, noisy3 = synth.noisy_image(4096, 4096, 2000, 1500, 30.0)
     rows3, r0 = 512, 1024
     band = torch.from_numpy(noisy3[r0 - 13:r0 + rows3 + 13]).cuda()
