@@ -53,3 +53,52 @@ def test_random_shapes_and_solvers_vs_oracle(oracle, seed):
         key = "anchored" if anchored else "plain"
         worst[key] = max(worst[key], d)
     assert worst["plain"] <= TOL
+
+
+@pytest.mark.parametrize("seed", [21])
+def test_random_batched_solves_vs_oracle(oracle, seed):
+    """Batched admm_euclidean_median / irls_euclidean_median on random shapes: d from 3 to 81
+    (reference-form, p-form, low-rank and generic kernels), n from 1 to 600 (both sides of the
+    448-point capacity of the low-rank kernels), mu 1e-3..10, 1..29 sweeps, box / unconstrained,
+    z_init / weighted mean, zero weights, clustered and uniform point sets at scale 1 and 255.
+    Minimisers within 1e-4 of the scale wherever the iteration counts agree (exact-stop ties of
+    the tol = 0 rule can differ between FP32 and FP64)."""
+    import paper_1501_03879_b200 as nb
+
+    rng = np.random.default_rng(seed)
+    compared = 0
+    for it in range(150):
+        d = int(rng.choice([3, 9, 17, 25, 30, 49, 49, 49, 81]))
+        n = int(rng.choice([1, 2, 3, 5, 25, 49, 121, 300, 441, 448, 449, 600]))
+        B = int(rng.choice([1, 3, 17, 64]))
+        mu = float(rng.choice([1.0, 0.1, 1e-3, 10.0]))
+        T = int(rng.integers(1, 30))
+        solver = str(rng.choice(["admm", "admm", "irls"]))
+        boxed = bool(rng.integers(0, 2))
+        scale = float(rng.choice([1.0, 255.0]))
+        kind = int(rng.integers(0, 3))
+        centre = rng.uniform(0, scale, (B, 1, d))
+        pts = (centre + rng.normal(0, 0.15 * scale, (B, n, d))) if kind else rng.uniform(0, scale, (B, n, d))
+        pts = pts.astype(np.float32)
+        w = rng.uniform(0.0, 1.0, (B, n)).astype(np.float32)
+        if kind == 2:
+            w[:, ::3] = 0.0
+        w[:, 0] = np.maximum(w[:, 0], 0.1)
+        zi = rng.uniform(0, scale, (B, d)).astype(np.float32) if rng.integers(0, 2) else None
+        box = (0.0, scale) if boxed else None
+        zi64 = None if zi is None else zi.astype(np.float64)
+        if solver == "admm":
+            gbox = nb.BoxConstraint.interval(*box) if box else nb.BoxConstraint.unconstrained()
+            r = nb.admm_euclidean_median(pts, w, gbox, nb.AdmmConfig(mu=mu, max_iter=T, z_init=zi))
+            ref = oracle.admm_batched(pts.astype(np.float64), w.astype(np.float64), mu=mu,
+                                      max_iter=T, box=box, z_init=zi64)
+        else:
+            eps = 1e-4 * scale * scale
+            r = nb.irls_euclidean_median(pts, w, nb.IrlsConfig(epsilon=eps, max_iter=T, tol=-1.0, x_init=zi))
+            ref = oracle.irls_batched(pts.astype(np.float64), w.astype(np.float64), epsilon=eps,
+                                      max_iter=T, tol=-1.0, x_init=zi64)
+        same = np.asarray(r.iterations_run) == np.asarray(ref.iterations)
+        err = np.abs(np.asarray(r.minimizer) - ref.minimizer).max(axis=1) / scale
+        assert (err[same] <= 1e-4).all(), (it, float(err[same].max()), solver, n, d, B, mu, T, boxed, scale, kind)
+        compared += int(same.sum())
+    assert compared > 1000
