@@ -102,3 +102,42 @@ def test_random_batched_solves_vs_oracle(oracle, seed):
         assert (err[same] <= 1e-4).all(), (it, float(err[same].max()), solver, n, d, B, mu, T, boxed, scale, kind)
         compared += int(same.sum())
     assert compared > 1000
+
+
+def test_random_band_splits_bitwise(oracle):
+    """Random row-band splits (1..4 bands, the caller's S/2 + k/2 halo, mirrored at the image
+    edges) through nlem_denoise_rows are bitwise the whole-image call for random shapes, kernels
+    and solvers - the multi-GPU contract, including the masked-window
+    kernels whose tile border exceeds the halo."""
+    import torch
+
+    import paper_1501_03879_b200 as nb
+
+    rng = np.random.default_rng(31)
+    for it in range(80):
+        k = int(rng.choice([3, 5, 7, 9]))
+        S = int(rng.choice(list(range(k, 24, 2))))
+        solver = str(rng.choice(["admm", "irls", "nlm_only"]))
+        mu = float(rng.choice([1.0, 1e-3]))
+        T = int(rng.integers(1, 14))
+        rows, cols = int(rng.integers(2, 60)), int(rng.integers(1, 50))
+        img = rng.uniform(0, 255, (rows, cols)).astype(np.float32)
+        p = nb.NlemParams(search=S, patch=k, h=200.0 * k, solver=solver, solver_iters=T, mu=mu,
+                          init_mode=str(rng.choice(["nlm", "noisy"])), epsilon=1e-4, irls_tol=-1.0)
+        X = torch.from_numpy(img).cuda()
+        whole = nb.nlem_denoise(X, p).cpu().numpy()
+        halo = S // 2 + k // 2
+        per = 2 * (rows - 1)
+
+        def mirror(i):
+            m = i % per
+            return m if m < rows else per - m
+
+        cuts = sorted({0, rows} | {int(c) for c in rng.integers(1, rows, size=int(rng.integers(1, 4)))})
+        parts = []
+        for r0, r1 in zip(cuts[:-1], cuts[1:]):
+            need = [mirror(r) for r in range(r0 - halo, r1 + halo)]
+            a0, a1 = min(need), max(need) + 1
+            parts.append(nb.nlem_denoise_rows(X[a0:a1].contiguous(), a0, rows, cols, r0, r1 - r0, p)
+                         .cpu().numpy())
+        assert np.array_equal(np.concatenate(parts), whole), (it, k, S, solver, mu, T, rows, cols, cuts)
