@@ -437,6 +437,9 @@ NLEM_LR_NAME(const float* __restrict__ pad, int pad_cols, int rows, int cols, in
     col[27] = 0.0f;
   }
   if (lane < SEGL + KS - 1) W[PB + 16 * PCS + 2 * lane + 1] = 0.0f;
+  // the transpose buffer's rows are summed unconditionally (rows a half does not write hold
+  // stale values whose sums every consumer masks): start from defined memory
+  for (int e = lane; e < 32 * RED_STR; e += 32) red[e] = 0.0f;
   if (idx < nidx) issue_tile(pix, 0);
 
 #ifdef NLEM_LR_STAMPS
